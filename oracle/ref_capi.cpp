@@ -218,10 +218,19 @@ int solve(void* h, const ref_spec* sp, int synthesize, V* values, V* residual,
     ErrOut e{err ? err->msg : nullptr, err ? 512 : 0, err ? reinterpret_cast<std::int64_t*>(&err->iterations) : nullptr,
              err ? &err->residual : nullptr, err ? &err->violation_kind : nullptr,
              err ? reinterpret_cast<std::int64_t*>(&err->violation_column) : nullptr};
+    auto* model = static_cast<Model<V>*>(static_cast<ModelBase*>(h));
+    // Problem holds the IMDP by value (property.hpp:73-77): move it in and back
+    // out so a timed solve does not pay for a model copy.
+    rimdp::Problem<V> problem{std::move(model->mdp), {}};
+    struct Restore {
+        Model<V>* m;
+        rimdp::Problem<V>* p;
+        ~Restore() { m->mdp = std::move(p->imdp); }
+    } restore{model, &problem};
     return guarded(e, [&] {
-        const auto& mdp = static_cast<Model<V>*>(static_cast<ModelBase*>(h))->mdp;
+        const auto& mdp = problem.imdp;
         const index_t n = mdp.num_states();
-        rimdp::Problem<V> problem{mdp, make_spec<V>(*sp, n)};
+        problem.spec = make_spec<V>(*sp, n);
         rimdp::SolverOptions opt;
         opt.workers = sp->workers;
         opt.max_iterations = sp->max_iterations;

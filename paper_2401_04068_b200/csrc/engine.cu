@@ -1,0 +1,813 @@
+// Host runtime of the B200 engine: device transition store, solve loop and
+// the extern "C" boundary declared in include/rimdp_b200.h.
+//
+// Replaces, for Value = double|float:
+//   IntervalMDP / IntervalProbabilities storage   imdp.hpp:26-181, interval.hpp:34-304
+//   detail::make_plan outputs (V0, frozen, ...)   solver.hpp:40-80 (built by the caller)
+//   detail::iterate                              solver.hpp:85-137
+//   detail::bellman_step_impl / bellman_step     bellman.hpp:75-133
+//   parallel_for_index (per-step thread fork)    parallel.hpp:27-68  -> CUDA grid
+#include "rimdp_b200.h"
+
+#include "omax_kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace rimdp_dev;
+
+namespace {
+
+thread_local std::string g_err_msg;
+thread_local rimdp_error_info g_err_info{};
+
+struct Fail {
+    int status;
+};
+
+int fail(int status, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err_msg = buf;
+    g_err_info = rimdp_error_info{};
+    g_err_info.status = status;
+    return status;
+}
+
+#define CK(expr)                                                                                          \
+    do {                                                                                                  \
+        cudaError_t e_ = (expr);                                                                          \
+        if (e_ != cudaSuccess) {                                                                          \
+            fail(e_ == cudaErrorMemoryAllocation ? RIMDP_ERR_OUT_OF_MEMORY : RIMDP_ERR_CUDA, "%s: %s (%s:%d)", \
+                 #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                                     \
+            throw Fail{g_err_info.status};                                                                \
+        }                                                                                                 \
+    } while (0)
+
+size_t elem_size(rimdp_dtype t) { return t == RIMDP_F64 ? 8 : 4; }
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        CK(cudaMalloc(&p, b > 0 ? b : 16));
+        bytes = b;
+    }
+    template <class U>
+    U* as() const { return static_cast<U*>(p); }
+};
+
+struct Infeasible {
+    int col;
+    int kind;
+    double sum;
+};
+
+struct SolveState {
+    DevBuf v[2], q, chosen, frozen, rewards, forced, res, ctl;
+    bool has_frozen = false, has_rewards = false, has_forced = false;
+    int forced_td = 0;
+    int pess = 1, maxi = 1, finite = 1;
+    long long horizon = 0, max_iterations = 0;
+    double eps = 0, discount = 0;
+    int chosen_td = 0;
+    long long launched = 0; // iterations enqueued so far
+    bool active = false;
+    bool record_only = false;
+    // kernel timing (rimdp_profile_*)
+    bool profile = false;
+    std::vector<cudaEvent_t> events;
+    size_t events_used = 0;
+    ~SolveState() {
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+    }
+    std::vector<int> host_frozen_copy; // for infeasible-column checks
+};
+
+} // namespace
+
+struct rimdp_model {
+    rimdp_dtype dtype = RIMDP_F64;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int n = 0;         // states owned by this store (local)
+    int n_global = 0;  // length of the value vector
+    int state_begin = 0;
+    int ncols = 0;
+    long long nnz = 0;
+    int maxlen = 0;
+    DevBuf stateptr, colptr, rows, lower, gap, rem, infeasible, quoted, short_list, long_list, scratch;
+    int nshort = 0, nlong = 0;
+    std::vector<int> h_stateptr;
+    std::vector<Infeasible> infeasible_cols;
+    long long device_bytes = 0;
+    int sm_count = 148;
+    SolveState s;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const Fail& e) {
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        return fail(RIMDP_ERR_OUT_OF_MEMORY, "host allocation failed");
+    } catch (...) {
+        return fail(RIMDP_ERR_INTERNAL, "unexpected exception");
+    }
+}
+
+int grid_for(long long work, int per_block, int sm_count, int blocks_per_sm) {
+    long long g = (work + per_block - 1) / per_block;
+    g = std::min<long long>(g, (long long)sm_count * blocks_per_sm);
+    return (int)std::max<long long>(g, 1);
+}
+
+// Column scheduler: route each column by length.
+void build_schedule(rimdp_model* m, const long long* h_colptr) {
+    std::vector<int> shortl, longl;
+    shortl.reserve(m->ncols);
+    int maxlen = 0;
+    for (int c = 0; c < m->ncols; ++c) {
+        const long long len = h_colptr[c + 1] - h_colptr[c];
+        maxlen = std::max<long long>(maxlen, len);
+        (len <= kShortLen ? shortl : longl).push_back(c);
+    }
+    m->maxlen = maxlen;
+    m->nshort = (int)shortl.size();
+    m->nlong = (int)longl.size();
+    m->short_list.ensure(sizeof(int) * std::max<size_t>(1, shortl.size()));
+    m->long_list.ensure(sizeof(int) * std::max<size_t>(1, longl.size()));
+    if (!shortl.empty())
+        CK(cudaMemcpyAsync(m->short_list.p, shortl.data(), sizeof(int) * shortl.size(), cudaMemcpyHostToDevice, m->stream));
+    if (!longl.empty())
+        CK(cudaMemcpyAsync(m->long_list.p, longl.data(), sizeof(int) * longl.size(), cudaMemcpyHostToDevice, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+}
+
+template <class T>
+void prepare(rimdp_model* m) {
+    m->rem.ensure(sizeof(T) * std::max(1, m->ncols));
+    m->infeasible.ensure(std::max(1, m->ncols));
+    m->quoted.ensure(sizeof(T) * std::max(1, m->ncols));
+    m->scratch.ensure(64);
+    CK(cudaMemsetAsync(m->scratch.p, 0, 64, m->stream));
+    int* counters = m->scratch.as<int>();
+    if (m->nnz > 0)
+        check_rows<<<grid_for(m->nnz, 256, m->sm_count, 8), 256, 0, m->stream>>>(m->nnz, m->rows.as<int>(), m->n_global,
+                                                                              counters + 1);
+    if (m->ncols > 0)
+        prepare_columns<T><<<grid_for(m->ncols, 128, m->sm_count, 16), 128, 0, m->stream>>>(
+            m->ncols, m->colptr.as<long long>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(),
+            m->infeasible.as<unsigned char>(), m->quoted.as<T>(), counters);
+    CK(cudaGetLastError());
+    int h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, counters, sizeof h, cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    if (h[1]) {
+        fail(RIMDP_ERR_INVALID_ARGUMENT, "row index out of range [0, %d)", m->n_global);
+        throw Fail{RIMDP_ERR_INVALID_ARGUMENT};
+    }
+    m->infeasible_cols.clear();
+    if (h[0]) {
+        std::vector<unsigned char> flags(m->ncols);
+        std::vector<T> sums(m->ncols);
+        CK(cudaMemcpy(flags.data(), m->infeasible.p, m->ncols, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sums.data(), m->quoted.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost));
+        for (int c = 0; c < m->ncols; ++c)
+            if (flags[c]) m->infeasible_cols.push_back({c, flags[c], (double)sums[c]});
+    }
+}
+
+void init_common(rimdp_model* m, int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        fail(RIMDP_ERR_NO_DEVICE, "no CUDA device visible");
+        throw Fail{RIMDP_ERR_NO_DEVICE};
+    }
+    if (device < 0 || device >= count) {
+        fail(RIMDP_ERR_INVALID_ARGUMENT, "device %d out of range (%d visible)", device, count);
+        throw Fail{RIMDP_ERR_INVALID_ARGUMENT};
+    }
+    m->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+}
+
+// ---------------------------------------------------------------------------
+// Solve loop
+
+template <class T>
+void upload_plan(rimdp_model* m, const rimdp_plan* p) {
+    SolveState& s = m->s;
+    const int N = m->n_global, n = m->n;
+    s.pess = p->pessimistic != 0;
+    s.maxi = p->maximize != 0;
+    s.finite = p->finite != 0;
+    s.horizon = p->horizon;
+    s.max_iterations = p->max_iterations;
+    s.eps = p->eps;
+    s.discount = p->discount;
+    s.v[0].ensure(sizeof(T) * N);
+    s.v[1].ensure(sizeof(T) * N);
+    s.q.ensure(sizeof(T) * std::max(1, m->ncols));
+    s.res.ensure(sizeof(T) * N);
+    s.ctl.ensure(sizeof(Ctl));
+    if (!p->initial) {
+        fail(RIMDP_ERR_INVALID_ARGUMENT, "plan.initial is required");
+        throw Fail{RIMDP_ERR_INVALID_ARGUMENT};
+    }
+    CK(cudaMemcpyAsync(s.v[0].p, p->initial, sizeof(T) * N, cudaMemcpyHostToDevice, m->stream));
+    CK(cudaMemcpyAsync(s.v[1].p, s.v[0].p, sizeof(T) * N, cudaMemcpyDeviceToDevice, m->stream));
+    s.has_frozen = p->frozen != nullptr;
+    s.host_frozen_copy.clear();
+    if (s.has_frozen) {
+        s.frozen.ensure(n);
+        CK(cudaMemcpyAsync(s.frozen.p, p->frozen + m->state_begin, n, cudaMemcpyHostToDevice, m->stream));
+        s.host_frozen_copy.assign(p->frozen + m->state_begin, p->frozen + m->state_begin + n);
+    }
+    s.has_rewards = p->rewards != nullptr;
+    if (s.has_rewards) {
+        s.rewards.ensure(sizeof(T) * n);
+        CK(cudaMemcpyAsync(s.rewards.p, static_cast<const T*>(p->rewards) + m->state_begin, sizeof(T) * n,
+                           cudaMemcpyHostToDevice, m->stream));
+    }
+    s.has_forced = p->forced != nullptr;
+    s.forced_td = p->forced_time_dependent != 0;
+    if (s.has_forced) {
+        const long long rows = s.forced_td ? std::max<long long>(p->horizon, 1) : 1;
+        s.forced.ensure(sizeof(int) * n * rows);
+        // local slice of each row
+        for (long long t = 0; t < rows; ++t)
+            CK(cudaMemcpyAsync(s.forced.as<int>() + t * n, p->forced + t * N + m->state_begin, sizeof(int) * n,
+                               cudaMemcpyHostToDevice, m->stream));
+    }
+    Ctl c{};
+    CK(cudaMemcpyAsync(s.ctl.p, &c, sizeof c, cudaMemcpyHostToDevice, m->stream));
+    s.launched = 0;
+    s.active = true;
+}
+
+template <class T>
+void launch_columns(rimdp_model* m, const T* V, T* q, Ctl* ctl, bool pess) {
+    if (m->nshort > 0) {
+        const int blocks = grid_for(m->nshort, kShortBatch * kWarpsPerBlock, m->sm_count, 6);
+        auto k = pess ? omax_short<T, true> : omax_short<T, false>;
+        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(m->nshort, m->short_list.as<int>(), m->colptr.as<long long>(),
+                                                          m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
+                                                          m->rem.as<T>(), V, q, ctl);
+    }
+    if (m->nlong > 0) {
+        const int blocks = grid_for(m->nlong, kWarpsPerBlock, m->sm_count, 8);
+        auto k = pess ? omax_long<T, true> : omax_long<T, false>;
+        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(m->nlong, m->long_list.as<int>(), m->colptr.as<long long>(),
+                                                         m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
+                                                         m->rem.as<T>(), V, q, ctl);
+    }
+}
+
+template <class T>
+void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
+    SolveState& s = m->s;
+    const T* vin = s.v[(k - 1) & 1].as<T>();
+    T* vout = s.v[k & 1].as<T>();
+    Ctl* ctl = s.ctl.as<Ctl>();
+    cudaEvent_t* ev = nullptr;
+    if (s.profile) {
+        while (s.events.size() < s.events_used + 3) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            s.events.push_back(e);
+        }
+        ev = &s.events[s.events_used];
+        s.events_used += 3;
+        CK(cudaEventRecord(ev[0], m->stream));
+    }
+    launch_columns<T>(m, vin, s.q.as<T>(), ctl, s.pess);
+    if (ev) CK(cudaEventRecord(ev[1], m->stream));
+    ActionArgs a{};
+    a.n = m->n;
+    a.state_begin = m->state_begin;
+    a.stateptr = m->stateptr.as<int>();
+    a.frozen = s.has_frozen ? s.frozen.as<unsigned char>() : nullptr;
+    a.forced = s.has_forced ? s.forced.as<int>() : nullptr;
+    a.forced_td = s.forced_td;
+    a.chosen = chosen;
+    a.chosen_td = chosen_td;
+    a.maximize = s.maxi;
+    a.finite = s.finite;
+    a.horizon = s.horizon;
+    a.max_iterations = s.max_iterations;
+    a.k = k;
+    a.record_only = s.record_only;
+    action_reduce<T><<<grid_for(m->n, 256, m->sm_count, 8), 256, 0, m->stream>>>(
+        a, s.q.as<T>(), vin, vout, s.has_rewards ? s.rewards.as<T>() : nullptr, (T)s.discount, (T)s.eps, ctl);
+    if (ev) CK(cudaEventRecord(ev[2], m->stream));
+    CK(cudaGetLastError());
+}
+
+int kernels_per_iteration(const rimdp_model* m) { return (m->nshort > 0) + (m->nlong > 0) + 1; }
+
+// First infeasible column that a step would evaluate (bellman.hpp:88-112:
+// frozen states are skipped, forced states evaluate one column; the lowest
+// state index wins, parallel.hpp:41-67).
+const Infeasible* first_evaluated_infeasible(rimdp_model* m, const rimdp_plan* p) {
+    if (m->infeasible_cols.empty()) return nullptr;
+    std::vector<char> bad(m->ncols, 0);
+    for (const auto& f : m->infeasible_cols) bad[f.col] = 1;
+    const int n = m->n, N = m->n_global;
+    auto lookup = [&](int c) -> const Infeasible* {
+        for (const auto& f : m->infeasible_cols)
+            if (f.col == c) return &f;
+        return nullptr;
+    };
+    const long long rows = (p->forced && p->forced_time_dependent) ? std::max<long long>(p->horizon, 1) : 1;
+    // iteration k = 1 uses row horizon - 1, k = 2 row horizon - 2, ...
+    for (long long it = 0; it < rows; ++it) {
+        const long long t = (p->forced && p->forced_time_dependent) ? p->horizon - 1 - it : 0;
+        for (int s = 0; s < n; ++s) {
+            if (p->frozen && p->frozen[m->state_begin + s]) continue;
+            int cb = m->h_stateptr[s], ce = m->h_stateptr[s + 1];
+            if (p->forced) {
+                const int f = p->forced[t * N + m->state_begin + s];
+                if (f >= 0) {
+                    cb = f;
+                    ce = f + 1;
+                }
+            }
+            for (int c = cb; c < ce; ++c)
+                if (bad[c]) return lookup(c);
+        }
+    }
+    return nullptr;
+}
+
+int report_infeasible(const Infeasible* f, rimdp_dtype dtype) {
+    char num[64];
+    // shortest round-trip text, as NumericTraits::to_string (numeric.hpp:30-35)
+    for (int prec = 1; prec <= 17; ++prec) {
+        snprintf(num, sizeof num, "%.*g", prec, f->sum);
+        const double back = strtod(num, nullptr);
+        if (dtype == RIMDP_F32 ? ((float)back == (float)f->sum) : (back == f->sum)) break;
+    }
+    fail(RIMDP_ERR_INFEASIBLE_COLUMN, "InfeasibleColumn: %s bounds sum to %s %s", f->kind == 1 ? "lower" : "upper",
+         num, f->kind == 1 ? "> 1" : "< 1");
+    g_err_info.column = f->col;
+    g_err_info.infeasible_kind = f->kind;
+    g_err_info.infeasible_sum = f->sum;
+    return RIMDP_ERR_INFEASIBLE_COLUMN;
+}
+
+template <class T>
+int solve_begin_t(rimdp_model* m, const rimdp_plan* p) {
+    upload_plan<T>(m, p);
+    return RIMDP_OK;
+}
+
+template <class T>
+void advance_t(rimdp_model* m, long long iters) {
+    SolveState& s = m->s;
+    int* chosen = nullptr;
+    int chosen_td = 0;
+    if (s.chosen.p) {
+        chosen = s.chosen.as<int>();
+        chosen_td = s.chosen_td;
+    }
+    for (long long i = 0; i < iters; ++i) {
+        const long long k = s.launched + 1;
+        if (s.finite && k > s.horizon) break;
+        if (!s.finite && k > s.max_iterations) break;
+        launch_iteration<T>(m, k, chosen, chosen_td);
+        s.launched = k;
+    }
+}
+
+Ctl read_ctl(rimdp_model* m) {
+    Ctl c{};
+    CK(cudaMemcpyAsync(&c, m->s.ctl.p, sizeof c, cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return c;
+}
+
+template <class T>
+void finish_t(rimdp_model* m, const rimdp_outputs* o, long long k) {
+    SolveState& s = m->s;
+    const int N = m->n_global;
+    if (o->values)
+        CK(cudaMemcpyAsync(o->values, s.v[k & 1].p, sizeof(T) * N, cudaMemcpyDeviceToHost, m->stream));
+    if (o->residual) {
+        if (k == 0) {
+            CK(cudaMemsetAsync(s.res.p, 0, sizeof(T) * N, m->stream));
+        } else {
+            residual_vector<T><<<grid_for(N, 256, m->sm_count, 8), 256, 0, m->stream>>>(N, s.v[k & 1].as<T>(),
+                                                                                        s.v[(k - 1) & 1].as<T>(),
+                                                                                        s.res.as<T>());
+            CK(cudaGetLastError());
+        }
+        CK(cudaMemcpyAsync(o->residual, s.res.p, sizeof(T) * N, cudaMemcpyDeviceToHost, m->stream));
+    }
+    if (o->chosen && s.chosen.p) {
+        const long long rows = s.chosen_td ? std::max<long long>(s.horizon, 0) : 1;
+        if (rows > 0)
+            CK(cudaMemcpyAsync(o->chosen, s.chosen.p, sizeof(int) * (size_t)m->n * rows, cudaMemcpyDeviceToHost,
+                               m->stream));
+    }
+    if (o->iterations) *o->iterations = k;
+    CK(cudaStreamSynchronize(m->stream));
+}
+
+void prepare_chosen(rimdp_model* m, const rimdp_outputs* o, const rimdp_plan* p) {
+    SolveState& s = m->s;
+    s.chosen_td = 0;
+    if (o && o->chosen) {
+        s.chosen_td = o->record_all_steps && p->finite;
+        const long long rows = s.chosen_td ? std::max<long long>(p->horizon, 1) : 1;
+        s.chosen.ensure(sizeof(int) * (size_t)m->n * rows);
+        CK(cudaMemsetAsync(s.chosen.p, 0xff, sizeof(int) * (size_t)m->n * rows, m->stream));
+    } else if (s.chosen.p) {
+        // keep the allocation but do not record
+        cudaFree(s.chosen.p);
+        s.chosen.p = nullptr;
+        s.chosen.bytes = 0;
+    }
+}
+
+template <class T>
+int solve_t(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
+    const bool will_step = p->finite ? p->horizon > 0 : true;
+    if (will_step) {
+        if (const Infeasible* f = first_evaluated_infeasible(m, p)) return report_infeasible(f, m->dtype);
+    }
+    m->s.record_only = false;
+    upload_plan<T>(m, p);
+    prepare_chosen(m, o, p);
+    const long long total = p->finite ? p->horizon : p->max_iterations;
+    long long k = 0;
+    Ctl c{};
+    if (o && o->on_iteration) {
+        std::vector<T> hv(m->n_global);
+        while (k < total) {
+            advance_t<T>(m, 1);
+            c = read_ctl(m);
+            k = c.k;
+            CK(cudaMemcpy(hv.data(), m->s.v[k & 1].p, sizeof(T) * m->n_global, cudaMemcpyDeviceToHost));
+            o->on_iteration(k, hv.data(), o->user);
+            if (c.done) break;
+        }
+    } else {
+        long long chunk = 8;
+        while (!c.done && m->s.launched < total) {
+            advance_t<T>(m, chunk);
+            c = read_ctl(m);
+            chunk = std::min<long long>(chunk * 2, 64);
+        }
+        k = c.k;
+    }
+    if (c.status == 2) return fail(RIMDP_ERR_INTERNAL, "partial-assignment overflow in a long column");
+    finish_t<T>(m, o, k);
+    m->s.active = false;
+    if (c.status == 1) {
+        fail(RIMDP_ERR_NON_CONVERGENCE, "no convergence after %lld iterations (max residual %f)", k, c.res_last);
+        g_err_info.iterations = k;
+        g_err_info.residual = c.res_last;
+        return RIMDP_ERR_NON_CONVERGENCE;
+    }
+    return RIMDP_OK;
+}
+
+template <class T>
+int step_t(rimdp_model* m, const void* v_in, int pess, int maxi, const uint8_t* frozen, const int32_t* forced,
+           void* v_out, int32_t* chosen_out) {
+    rimdp_plan p{};
+    p.pessimistic = pess;
+    p.maximize = maxi;
+    p.finite = 1;
+    p.horizon = 1;
+    p.initial = v_in;
+    p.frozen = frozen;
+    p.forced = forced;
+    if (const Infeasible* f = first_evaluated_infeasible(m, &p)) return report_infeasible(f, m->dtype);
+    rimdp_outputs o{};
+    o.values = v_out;
+    o.chosen = chosen_out;
+    m->s.record_only = false;
+    upload_plan<T>(m, &p);
+    prepare_chosen(m, &o, &p);
+    advance_t<T>(m, 1);
+    finish_t<T>(m, &o, 1);
+    return RIMDP_OK;
+}
+
+template <class T>
+int column_values_t(rimdp_model* m, const void* v_in, int pess, void* q_out) {
+    SolveState& s = m->s;
+    s.v[0].ensure(sizeof(T) * m->n_global);
+    s.q.ensure(sizeof(T) * std::max(1, m->ncols));
+    CK(cudaMemcpyAsync(s.v[0].p, v_in, sizeof(T) * m->n_global, cudaMemcpyHostToDevice, m->stream));
+    launch_columns<T>(m, s.v[0].as<T>(), s.q.as<T>(), nullptr, pess != 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(q_out, s.q.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return RIMDP_OK;
+}
+
+#define DISPATCH(m, fn, ...) ((m)->dtype == RIMDP_F64 ? fn<double>(__VA_ARGS__) : fn<float>(__VA_ARGS__))
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char* rimdp_last_error(void) { return g_err_msg.c_str(); }
+
+int rimdp_last_error_info(rimdp_error_info* out) {
+    if (!out) return RIMDP_ERR_INVALID_ARGUMENT;
+    *out = g_err_info;
+    return RIMDP_OK;
+}
+
+int rimdp_abi_version(void) { return RIMDP_B200_ABI_VERSION; }
+
+int rimdp_device_count(int* count) {
+    if (!count) return fail(RIMDP_ERR_INVALID_ARGUMENT, "count is null");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+    *count = c;
+    return RIMDP_OK;
+}
+
+int rimdp_model_create(const rimdp_model_desc* d, rimdp_model** out) {
+    return guarded([&]() -> int {
+        if (!d || !out) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+        if (d->dtype != RIMDP_F64 && d->dtype != RIMDP_F32) return fail(RIMDP_ERR_INVALID_ARGUMENT, "unknown dtype");
+        if (d->num_states < 0 || d->num_cols < 0 || d->nnz < 0 || !d->stateptr || !d->colptr)
+            return fail(RIMDP_ERR_INVALID_ARGUMENT, "bad model sizes");
+        if (d->nnz > 0 && (!d->rowval || !d->lower || !d->upper))
+            return fail(RIMDP_ERR_INVALID_ARGUMENT, "null CSC arrays");
+        // structural checks of the pointer arrays (csc.hpp:76-106, imdp.hpp:129-168)
+        if (d->colptr[0] != 0 || d->colptr[d->num_cols] != d->nnz)
+            return fail(RIMDP_ERR_INVALID_ARGUMENT, "colptr must run from 0 to nnz");
+        for (int c = 0; c < d->num_cols; ++c)
+            if (d->colptr[c + 1] < d->colptr[c]) return fail(RIMDP_ERR_INVALID_ARGUMENT, "colptr not monotone at %d", c);
+        if (d->stateptr[0] != 0 || d->stateptr[d->num_states] != d->num_cols)
+            return fail(RIMDP_ERR_INVALID_ARGUMENT, "stateptr must run from 0 to num_cols");
+        for (int s = 0; s < d->num_states; ++s)
+            if (d->stateptr[s + 1] < d->stateptr[s])
+                return fail(RIMDP_ERR_INVALID_ARGUMENT, "stateptr not monotone at %d", s);
+        std::unique_ptr<rimdp_model> m(new rimdp_model);
+        m->dtype = d->dtype;
+        init_common(m.get(), d->device);
+        DeviceGuard g(m->device);
+        m->n = m->n_global = d->num_states;
+        m->ncols = d->num_cols;
+        m->nnz = d->nnz;
+        m->h_stateptr.assign(d->stateptr, d->stateptr + d->num_states + 1);
+        const size_t es = elem_size(d->dtype);
+        m->stateptr.ensure(sizeof(int) * (d->num_states + 1));
+        m->colptr.ensure(sizeof(long long) * (d->num_cols + 1));
+        m->rows.ensure(sizeof(int) * std::max<long long>(1, d->nnz));
+        m->lower.ensure(es * std::max<long long>(1, d->nnz));
+        m->gap.ensure(es * std::max<long long>(1, d->nnz));
+        CK(cudaMemcpyAsync(m->stateptr.p, d->stateptr, sizeof(int) * (d->num_states + 1), cudaMemcpyHostToDevice,
+                           m->stream));
+        CK(cudaMemcpyAsync(m->colptr.p, d->colptr, sizeof(long long) * (d->num_cols + 1), cudaMemcpyHostToDevice,
+                           m->stream));
+        if (d->nnz > 0) {
+            CK(cudaMemcpyAsync(m->rows.p, d->rowval, sizeof(int) * d->nnz, cudaMemcpyHostToDevice, m->stream));
+            CK(cudaMemcpyAsync(m->lower.p, d->lower, es * d->nnz, cudaMemcpyHostToDevice, m->stream));
+            CK(cudaMemcpyAsync(m->gap.p, d->upper, es * d->nnz, cudaMemcpyHostToDevice, m->stream));
+        }
+        build_schedule(m.get(), reinterpret_cast<const long long*>(d->colptr));
+        DISPATCH(m, prepare, m.get());
+        m->device_bytes = (long long)(m->stateptr.bytes + m->colptr.bytes + m->rows.bytes + m->lower.bytes +
+                                      m->gap.bytes + m->rem.bytes + m->infeasible.bytes + m->quoted.bytes +
+                                      m->short_list.bytes + m->long_list.bytes);
+        *out = m.release();
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_model_destroy(rimdp_model* m) {
+    if (!m) return RIMDP_OK;
+    {
+        DeviceGuard g(m->device);
+        if (m->stream) cudaStreamSynchronize(m->stream);
+        m->s.~SolveState();
+        new (&m->s) SolveState();
+        if (m->stream) cudaStreamDestroy(m->stream);
+        m->stream = nullptr;
+    }
+    delete m;
+    return RIMDP_OK;
+}
+
+int rimdp_model_info_get(rimdp_model* m, rimdp_model_info* o) {
+    if (!m || !o) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    *o = rimdp_model_info{};
+    o->dtype = m->dtype;
+    o->device = m->device;
+    o->num_states = m->n;
+    o->num_cols = m->ncols;
+    o->nnz = m->nnz;
+    o->state_begin = m->state_begin;
+    o->state_end = m->state_begin + m->n;
+    o->max_column_length = m->maxlen;
+    o->num_infeasible_columns = (int)m->infeasible_cols.size();
+    o->device_bytes = m->device_bytes;
+    o->short_columns = m->nshort;
+    o->mid_columns = 0;
+    o->long_columns = m->nlong;
+    return RIMDP_OK;
+}
+
+int rimdp_model_stream(rimdp_model* m, void** s) {
+    if (!m || !s) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    *s = m->stream;
+    return RIMDP_OK;
+}
+
+static int check_plan(rimdp_model* m, const rimdp_plan* p) {
+    if (!m || !p) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    if (!p->initial) return fail(RIMDP_ERR_INVALID_ARGUMENT, "plan.initial is required");
+    if (p->finite && p->horizon < 0) return fail(RIMDP_ERR_INVALID_ARGUMENT, "negative horizon");
+    if (p->forced) {
+        const long long rows = p->forced_time_dependent ? p->horizon : 1;
+        for (long long t = 0; t < rows; ++t)
+            for (int s = 0; s < m->n; ++s) {
+                const int f = p->forced[t * m->n_global + m->state_begin + s];
+                if (f >= 0 && (f < m->h_stateptr[s] || f >= m->h_stateptr[s + 1]))
+                    return fail(RIMDP_ERR_INVALID_ARGUMENT, "forced column %d is not a column of state %d", f,
+                                m->state_begin + s);
+            }
+    }
+    return RIMDP_OK;
+}
+
+int rimdp_solve(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
+    if (int st = check_plan(m, p)) return st;
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        rimdp_outputs none{};
+        return DISPATCH(m, solve_t, m, p, o ? o : &none);
+    });
+}
+
+int rimdp_solve_begin(rimdp_model* m, const rimdp_plan* p) {
+    if (int st = check_plan(m, p)) return st;
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        m->s.record_only = false;
+        rimdp_outputs none{};
+        prepare_chosen(m, &none, p);
+        return DISPATCH(m, solve_begin_t, m, p);
+    });
+}
+
+int rimdp_solve_advance(rimdp_model* m, int64_t iters) {
+    if (!m || !m->s.active) return fail(RIMDP_ERR_INVALID_ARGUMENT, "no active solve");
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        if (m->dtype == RIMDP_F64)
+            advance_t<double>(m, iters);
+        else
+            advance_t<float>(m, iters);
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_solve_poll(rimdp_model* m, int64_t* k, int32_t* finished, double* res) {
+    if (!m || !m->s.active) return fail(RIMDP_ERR_INVALID_ARGUMENT, "no active solve");
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        Ctl c = read_ctl(m);
+        if (k) *k = c.k;
+        if (finished) *finished = c.done;
+        if (res) *res = c.res_last;
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_solve_finish(rimdp_model* m, const rimdp_outputs* o) {
+    if (!m || !m->s.active) return fail(RIMDP_ERR_INVALID_ARGUMENT, "no active solve");
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        Ctl c = read_ctl(m);
+        rimdp_outputs none{};
+        if (m->dtype == RIMDP_F64)
+            finish_t<double>(m, o ? o : &none, c.k);
+        else
+            finish_t<float>(m, o ? o : &none, c.k);
+        m->s.active = false;
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_profile_enable(rimdp_model* m, int32_t on) {
+    if (!m) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null model");
+    m->s.profile = on != 0;
+    return RIMDP_OK;
+}
+
+int rimdp_profile_read(rimdp_model* m, double* column_ms, double* action_ms, int64_t* iterations,
+                       int32_t* kernels) {
+    if (!m) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null model");
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        CK(cudaStreamSynchronize(m->stream));
+        double c = 0, a = 0;
+        long long it = 0;
+        for (size_t i = 0; i + 3 <= m->s.events_used; i += 3) {
+            float x = 0, y = 0;
+            CK(cudaEventElapsedTime(&x, m->s.events[i], m->s.events[i + 1]));
+            CK(cudaEventElapsedTime(&y, m->s.events[i + 1], m->s.events[i + 2]));
+            c += x;
+            a += y;
+            ++it;
+        }
+        m->s.events_used = 0;
+        if (column_ms) *column_ms = c;
+        if (action_ms) *action_ms = a;
+        if (iterations) *iterations = it;
+        if (kernels) *kernels = kernels_per_iteration(m);
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_solve_value_buffers(rimdp_model* m, void** b0, void** b1) {
+    if (!m || !m->s.active) return fail(RIMDP_ERR_INVALID_ARGUMENT, "no active solve");
+    if (b0) *b0 = m->s.v[0].p;
+    if (b1) *b1 = m->s.v[1].p;
+    return RIMDP_OK;
+}
+
+int rimdp_bellman_step(rimdp_model* m, const void* v_in, int32_t pess, int32_t maxi, const uint8_t* frozen,
+                       const int32_t* forced, void* v_out, int32_t* chosen_out) {
+    if (!m || !v_in || !v_out) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    rimdp_plan p{};
+    p.initial = v_in;
+    p.forced = forced;
+    p.finite = 1;
+    p.horizon = 1;
+    if (int st = check_plan(m, &p)) return st;
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        return DISPATCH(m, step_t, m, v_in, pess, maxi, frozen, forced, v_out, chosen_out);
+    });
+}
+
+int rimdp_column_values(rimdp_model* m, const void* v_in, int32_t pess, void* q_out) {
+    if (!m || !v_in || !q_out) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        return DISPATCH(m, column_values_t, m, v_in, pess, q_out);
+    });
+}
+
+int rimdp_model_generate(const rimdp_gen_config* cfg, rimdp_model** out) {
+    (void)cfg;
+    (void)out;
+    return fail(RIMDP_ERR_INTERNAL, "rimdp_model_generate: not built in this configuration");
+}
+
+int rimdp_model_read_columns(rimdp_model* m, int32_t cb, int32_t ce, int64_t* colptr_out, int32_t* rowval_out,
+                             void* lower_out, void* upper_out) {
+    (void)m; (void)cb; (void)ce; (void)colptr_out; (void)rowval_out; (void)lower_out; (void)upper_out;
+    return fail(RIMDP_ERR_INTERNAL, "rimdp_model_read_columns: not built in this configuration");
+}
+
+} // extern "C"

@@ -1,0 +1,68 @@
+// Scalar policy for the device kernels: explicit round-to-nearest operations
+// (no FMA contraction, so every multiply and add rounds exactly like the
+// reference built for x86-64 without -march), the feasibility tolerance of
+// NumericTraits (numeric.hpp:53-81), and an order-preserving integer key for
+// the adversary ordering of omax.hpp:41-58.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rimdp_dev {
+
+template <class T>
+struct Num;
+
+template <>
+struct Num<double> {
+    using Bits = unsigned long long;
+    static constexpr int kKeyWords = 2;
+    __host__ __device__ static double tol() { return 1e-9; }
+    __device__ __forceinline__ static double add(double a, double b) { return __dadd_rn(a, b); }
+    __device__ __forceinline__ static double sub(double a, double b) { return __dsub_rn(a, b); }
+    __device__ __forceinline__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+    // Value -> unsigned key whose integer order is the ordering the reference
+    // sorts by: ascending V for the pessimistic adversary, descending for the
+    // optimistic one.  -0.0 and +0.0 map to the same key because the
+    // reference compares values with != (ties then fall back to the row).
+    __device__ __forceinline__ static Bits key(double v, bool pessimistic) {
+        Bits b = static_cast<Bits>(__double_as_longlong(v == 0.0 ? 0.0 : v));
+        b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+        return pessimistic ? b : ~b;
+    }
+    // Non-negative residuals compare like their bit patterns.
+    __device__ __forceinline__ static unsigned long long res_bits(double r) {
+        return static_cast<unsigned long long>(__double_as_longlong(r));
+    }
+    __host__ __device__ static double from_res_bits(unsigned long long b) {
+        double d;
+        memcpy(&d, &b, sizeof d);
+        return d;
+    }
+};
+
+template <>
+struct Num<float> {
+    using Bits = unsigned int;
+    static constexpr int kKeyWords = 1;
+    __host__ __device__ static float tol() { return 1e-5f; }
+    __device__ __forceinline__ static float add(float a, float b) { return __fadd_rn(a, b); }
+    __device__ __forceinline__ static float sub(float a, float b) { return __fsub_rn(a, b); }
+    __device__ __forceinline__ static float mul(float a, float b) { return __fmul_rn(a, b); }
+    __device__ __forceinline__ static Bits key(float v, bool pessimistic) {
+        Bits b = static_cast<Bits>(__float_as_int(v == 0.0f ? 0.0f : v));
+        b = (b >> 31) ? ~b : (b | 0x80000000u);
+        return pessimistic ? b : ~b;
+    }
+    __device__ __forceinline__ static unsigned long long res_bits(float r) {
+        return static_cast<unsigned long long>(static_cast<unsigned>(__float_as_int(r)));
+    }
+    __host__ __device__ static float from_res_bits(unsigned long long b) {
+        unsigned u = static_cast<unsigned>(b);
+        float f;
+        memcpy(&f, &u, sizeof f);
+        return f;
+    }
+};
+
+} // namespace rimdp_dev

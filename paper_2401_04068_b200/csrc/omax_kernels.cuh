@@ -1,0 +1,406 @@
+// sm_100a kernels of the robust Bellman operator.
+//
+// Reference semantics (proj/include/rimdp/, all f64/f32 paths):
+//   per column   omax_remainder (omax.hpp:64-85)  — precomputed once per model
+//                value_ordering (omax.hpp:41-58) / column_value (bellman.hpp:60-70)
+//                omaximize_sequential (omax.hpp:98-112)
+//                row-order dot (omax.hpp:169-173)
+//   per state    bellman_step_impl (bellman.hpp:75-118)
+//   per iterate  reward update, residual, stop test (solver.hpp:107-134)
+//
+// Every floating-point operation the reference performs is performed here
+// in the same order with the same rounding, so results are bit-identical:
+//   * the adversary ordering is found by exact integer argmin over
+//     (order-preserving key of V[row], position) — position order is row
+//     order because rows are strictly increasing (csc.hpp:98-101);
+//   * `consumed` is accumulated sequentially along that ordering;
+//   * the expectation is summed sequentially in row order by one lane per
+//     column, from products staged in shared memory.
+#pragma once
+
+#include "numeric.cuh"
+
+#include <climits>
+#include <cstdint>
+
+namespace rimdp_dev {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kShortLen = 32;        // columns with <= 32 entries: one lane per entry
+constexpr int kShortBatch = 16;      // columns per warp batch in the short kernel
+constexpr int kWarpsPerBlock = 8;
+constexpr int kMaxPartial = 4;       // partially-filled positions tracked per long column
+
+// Device loop state of one solve.
+struct Ctl {
+    unsigned long long res_bits[2]; // max residual of iteration k, slot k & 1
+    unsigned int arrive;            // blocks of the action kernel that finished
+    int done;                       // stop condition reached; later launches are no-ops
+    int status;                     // 0 ok, 1 non-convergence, 2 internal
+    int pad;
+    long long k;                    // iterations completed
+    double res_last;                // max residual of the last iteration, as double
+};
+
+// ---------------------------------------------------------------------------
+// Model preparation: per-column remainder and feasibility (omax.hpp:64-85),
+// and gap = upper - lower in place of upper.  Sequential in row order, so the
+// sums carry the reference's rounding.
+template <class T>
+__global__ void prepare_columns(int ncols, const long long* __restrict__ colptr, const T* __restrict__ lower,
+                                T* __restrict__ upper_to_gap, T* __restrict__ rem, unsigned char* __restrict__ infeasible,
+                                T* __restrict__ quoted_sum, int* __restrict__ n_infeasible) {
+    using N = Num<T>;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+        const long long b = colptr[c], e = colptr[c + 1];
+        T ls = T(0), gs = T(0);
+        for (long long i = b; i < e; ++i) {
+            const T g = N::sub(upper_to_gap[i], lower[i]);
+            ls = N::add(ls, lower[i]);
+            gs = N::add(gs, g);
+            upper_to_gap[i] = g;
+        }
+        unsigned char bad = 0;
+        T q = T(0);
+        if (ls > N::add(T(1), N::tol())) {
+            bad = 1;
+            q = ls;
+        } else if (N::add(ls, gs) < N::sub(T(1), N::tol())) {
+            bad = 2;
+            q = N::add(ls, gs);
+        }
+        T r = N::sub(T(1), ls);
+        if (r < T(0)) r = T(0);
+        if (r > gs) r = gs;
+        rem[c] = r;
+        infeasible[c] = bad;
+        quoted_sum[c] = q;
+        if (bad) atomicAdd(n_infeasible, 1);
+    }
+}
+
+__global__ void check_rows(long long nnz, const int* __restrict__ rows, int n, int* __restrict__ bad) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nnz; i += (long long)gridDim.x * blockDim.x) {
+        const int r = rows[i];
+        if (r < 0 || r >= n) atomicExch(bad, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-wide exact argmin helpers.
+
+// Lane holding the smallest (key, lane) among lanes with `active`, or -1.
+template <class Bits>
+__device__ __forceinline__ int warp_argmin_lane(Bits key, bool active) {
+    if (__ballot_sync(kFull, active) == 0u) return -1;
+    bool cand = active;
+    if constexpr (sizeof(Bits) == 8) {
+        const unsigned hi = static_cast<unsigned>(key >> 32);
+        const unsigned mhi = __reduce_min_sync(kFull, active ? hi : 0xffffffffu);
+        cand = cand && hi == mhi;
+        const unsigned lo = static_cast<unsigned>(key);
+        const unsigned mlo = __reduce_min_sync(kFull, cand ? lo : 0xffffffffu);
+        cand = cand && lo == mlo;
+    } else {
+        const unsigned mk = __reduce_min_sync(kFull, active ? static_cast<unsigned>(key) : 0xffffffffu);
+        cand = cand && static_cast<unsigned>(key) == mk;
+    }
+    return __ffs(__ballot_sync(kFull, cand)) - 1;
+}
+
+// Smallest (key, pos) over lanes with `active`; returns false when none.
+template <class Bits>
+__device__ __forceinline__ bool warp_argmin_pos(Bits key, int pos, bool active, Bits& kout, int& pout) {
+    if (__ballot_sync(kFull, active) == 0u) return false;
+    bool cand = active;
+    Bits k;
+    if constexpr (sizeof(Bits) == 8) {
+        const unsigned hi = static_cast<unsigned>(key >> 32);
+        const unsigned mhi = __reduce_min_sync(kFull, active ? hi : 0xffffffffu);
+        cand = cand && hi == mhi;
+        const unsigned lo = static_cast<unsigned>(key);
+        const unsigned mlo = __reduce_min_sync(kFull, cand ? lo : 0xffffffffu);
+        cand = cand && lo == mlo;
+        k = (static_cast<Bits>(mhi) << 32) | mlo;
+    } else {
+        const unsigned mk = __reduce_min_sync(kFull, active ? static_cast<unsigned>(key) : 0xffffffffu);
+        cand = cand && static_cast<unsigned>(key) == mk;
+        k = mk;
+    }
+    pout = static_cast<int>(__reduce_min_sync(kFull, cand ? static_cast<unsigned>(pos) : 0xffffffffu));
+    kout = k;
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Short columns (<= 32 entries).  A warp takes 16 columns at a time.  For
+// each column, lane i owns entry i: coalesced loads, one V gather, and the
+// greedy assignment driven by exact warp argmins (one per position that
+// receives mass; typically 1-3).  Products V[row_i] * p_i go to shared
+// memory; then lane t sums column t's products sequentially in row order.
+template <class T, bool kPess>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+omax_short(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+           const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+           const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    __shared__ T xs[kWarpsPerBlock][kShortBatch][kShortLen + 1];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
+    for (int base = gw * kShortBatch; base < nlist; base += nw * kShortBatch) {
+        const int mine = base + (lane & (kShortBatch - 1));
+        int c = -1;
+        long long beg = 0;
+        int len = 0;
+        T crem = T(0);
+        if (lane < kShortBatch && mine < nlist) {
+            c = list[mine];
+            beg = colptr[c];
+            len = static_cast<int>(colptr[c + 1] - beg);
+            crem = rem[c];
+        }
+        const int ncol = min(kShortBatch, nlist - base);
+        for (int k = 0; k < ncol; ++k) {
+            const long long b = __shfl_sync(kFull, beg, k);
+            const int L = __shfl_sync(kFull, len, k);
+            const T r = __shfl_sync(kFull, crem, k);
+            const bool valid = lane < L;
+            T l = T(0), g = T(0), v = T(0);
+            if (valid) {
+                const int row = __ldg(rows + b + lane);
+                l = __ldg(lower + b + lane);
+                g = __ldg(gap + b + lane);
+                v = __ldg(V + row);
+            }
+            T p = l;
+            const Bits key = N::key(v, kPess);
+            bool active = valid;
+            T consumed = T(0);
+            for (;;) {
+                const T avail = N::sub(r, consumed);
+                if (!(avail > T(0))) break;
+                const int sel = warp_argmin_lane(key, active);
+                if (sel < 0) break;
+                const T gs = __shfl_sync(kFull, g, sel);
+                if (lane == sel) {
+                    p = N::add(l, g < avail ? g : avail);
+                    active = false;
+                }
+                consumed = N::add(consumed, gs);
+            }
+            if (valid) xs[w][k][lane] = N::mul(v, p);
+        }
+        __syncwarp();
+        if (c >= 0) {
+            T acc = T(0);
+            for (int i = 0; i < len; ++i) acc = N::add(acc, xs[w][lane][i]);
+            q[c] = acc;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Long columns (> 32 entries).  One warp per column.  Each greedy step is a
+// warp argmin over the entries strictly after the previous pick in the
+// adversary ordering; only positions whose assignment is clipped by the
+// remaining mass (g >= avail) need their value remembered, every other
+// picked position receives lower + gap.  The expectation is then summed in
+// row order, 32 products at a time, by lane 0.
+template <class T, bool kPess>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+          const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+          const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, Ctl* __restrict__ ctl) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    __shared__ T xs[kWarpsPerBlock][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
+    for (int i = gw; i < nlist; i += nw) {
+        const int c = list[i];
+        const long long b = colptr[c];
+        const int L = static_cast<int>(colptr[c + 1] - b);
+        const T r = rem[c];
+        // greedy along the adversary ordering
+        bool any = false;
+        Bits lastk = 0;
+        int lastp = -1;
+        int npart = 0;
+        int ppos[kMaxPartial];
+        T pval[kMaxPartial];
+        T consumed = T(0);
+        for (;;) {
+            const T avail = N::sub(r, consumed);
+            if (!(avail > T(0))) break;
+            Bits bk = ~Bits(0);
+            int bp = INT_MAX;
+            bool have = false;
+            for (int j = lane; j < L; j += 32) {
+                const Bits k = N::key(__ldg(V + __ldg(rows + b + j)), kPess);
+                const bool after = !any || k > lastk || (k == lastk && j > lastp);
+                if (after && (!have || k < bk || (k == bk && j < bp))) {
+                    bk = k;
+                    bp = j;
+                    have = true;
+                }
+            }
+            Bits mk;
+            int mp;
+            if (!warp_argmin_pos(bk, bp, have, mk, mp)) break;
+            const T g = __ldg(gap + b + mp);
+            if (!(g < avail)) {
+                if (npart < kMaxPartial) {
+                    ppos[npart] = mp;
+                    pval[npart] = N::add(__ldg(lower + b + mp), avail);
+                }
+                ++npart;
+            }
+            consumed = N::add(consumed, g);
+            any = true;
+            lastk = mk;
+            lastp = mp;
+        }
+        if (npart > kMaxPartial && lane == 0) atomicExch(&ctl->status, 2);
+        // expectation in row order
+        T acc = T(0);
+        for (int j0 = 0; j0 < L; j0 += 32) {
+            const int j = j0 + lane;
+            T x = T(0);
+            if (j < L) {
+                const T v = __ldg(V + __ldg(rows + b + j));
+                const T l = __ldg(lower + b + j);
+                T p = l;
+                if (any) {
+                    const Bits k = N::key(v, kPess);
+                    if (k < lastk || (k == lastk && j <= lastp)) {
+                        p = N::add(l, __ldg(gap + b + j));
+                        for (int t = 0; t < npart && t < kMaxPartial; ++t)
+                            if (ppos[t] == j) p = pval[t];
+                    }
+                }
+                x = N::mul(v, p);
+            }
+            xs[w][lane] = x;
+            __syncwarp();
+            if (lane == 0) {
+                const int m = min(32, L - j0);
+                for (int t = 0; t < m; ++t) acc = N::add(acc, xs[w][t]);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) q[c] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Action reduction + reach/avoid/discount update + residual + stop test, one
+// thread per state (bellman.hpp:88-115, solver.hpp:107-134).  The block max
+// of |V_k - V_{k-1}| is folded with one atomicMax; the last block to finish
+// evaluates the stop test for iteration k, so the residual needs no extra
+// pass and the host needs no per-iteration synchronisation.
+struct ActionArgs {
+    int n;
+    int state_begin;               // shard offset of local state 0 in the global value vector
+    const int* stateptr;           // local columns of local states
+    const unsigned char* frozen;   // local [n] or null
+    const int* forced;             // null, [n], or [horizon][n]
+    int forced_td;
+    int* chosen;                   // [n] or [horizon][n]
+    int chosen_td;
+    int maximize;
+    int finite;
+    long long horizon;
+    long long max_iterations;
+    long long k;                   // the iteration this launch computes (1-based)
+    int record_only;               // sharded solves: the driver owns the stop test
+};
+
+template <class T>
+__global__ void __launch_bounds__(256)
+action_reduce(ActionArgs a, const T* __restrict__ q, const T* __restrict__ vin, T* __restrict__ vout,
+              const T* __restrict__ rewards, T discount, T eps, Ctl* __restrict__ ctl) {
+    using N = Num<T>;
+    if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    const int* forced = a.forced ? a.forced + (a.forced_td ? (a.horizon - a.k) * (long long)a.n : 0) : nullptr;
+    int* chosen = a.chosen ? a.chosen + (a.chosen_td ? (a.horizon - a.k) * (long long)a.n : 0) : nullptr;
+    unsigned long long my = 0;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.n; s += gridDim.x * blockDim.x) {
+        const T prev = vin[a.state_begin + s];
+        T best;
+        int best_c = -1;
+        if (a.frozen && a.frozen[s]) {
+            best = prev;
+        } else {
+            int cb = a.stateptr[s], ce = a.stateptr[s + 1];
+            if (forced && forced[s] >= 0) {
+                cb = forced[s];
+                ce = cb + 1;
+            }
+            best = cb < ce ? q[cb] : prev; // a state without columns keeps its value
+            best_c = cb < ce ? cb : -1;
+            for (int c = cb + 1; c < ce; ++c) {
+                const T x = q[c];
+                if (a.maximize ? (x > best) : (x < best)) {
+                    best = x;
+                    best_c = c;
+                }
+            }
+        }
+        if (rewards) best = N::add(rewards[s], N::mul(discount, best));
+        vout[a.state_begin + s] = best;
+        if (chosen) chosen[s] = best_c;
+        const T res = fabs(N::sub(best, prev));
+        const unsigned long long rb = N::res_bits(res);
+        my = rb > my ? rb : my;
+    }
+    // block max -> one atomic per block
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(kFull, my, o);
+        my = other > my ? other : my;
+    }
+    __shared__ unsigned long long wmax[8];
+    __shared__ bool last;
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = my;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = wmax[i] > m ? wmax[i] : m;
+        if (m) atomicMax(&ctl->res_bits[a.k & 1], m);
+        __threadfence();
+        last = atomicAdd(&ctl->arrive, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long rb = atomicAdd(&ctl->res_bits[a.k & 1], 0ull);
+        const T res = N::from_res_bits(rb);
+        ctl->k = a.k;
+        ctl->res_last = static_cast<double>(res);
+        ctl->res_bits[(a.k + 1) & 1] = 0ull;
+        ctl->arrive = 0u;
+        if (a.record_only) {
+            // global residual is reduced across ranks by the sharded driver
+        } else if (a.finite) {
+            if (a.k >= a.horizon) ctl->done = 1;
+        } else if (res <= eps) {
+            ctl->done = 1;
+        } else if (a.k >= a.max_iterations) {
+            ctl->done = 1;
+            ctl->status = 1;
+        }
+        __threadfence();
+    }
+}
+
+template <class T>
+__global__ void residual_vector(int n, const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out) {
+    using N = Num<T>;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x)
+        out[s] = fabs(N::sub(a[s], b[s]));
+}
+
+} // namespace rimdp_dev

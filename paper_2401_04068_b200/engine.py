@@ -1,0 +1,300 @@
+"""ctypes binding of the C ABI in include/rimdp_b200.h.
+
+This is plumbing for tests, bench.py and the sharded driver; the drop-in
+host API for C++ callers is include/rimdp/*.hpp.  The library is loaded from
+the package tree (``lib/librimdp_b200.so``); there is no CPU fallback — if
+the library is missing, building or loading raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import build as _build
+
+RIMDP_F64, RIMDP_F32 = 0, 1
+OK, ERR_INVALID_ARGUMENT, ERR_INFEASIBLE_COLUMN, ERR_NON_CONVERGENCE, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE, ERR_INTERNAL = range(8)
+
+
+class EngineError(RuntimeError):
+    """A non-zero rimdp_status with the thread's rimdp_last_error() text."""
+
+    def __init__(self, status: int, message: str, info: "ErrorInfo"):
+        self.status = status
+        self.message = message
+        self.iterations = int(info.iterations)
+        self.residual = float(info.residual)
+        self.column = int(info.column)
+        super().__init__(f"rimdp status {status}: {message}")
+
+
+class ErrorInfo(C.Structure):
+    _fields_ = [("status", C.c_int32), ("iterations", C.c_int64), ("residual", C.c_double),
+                ("column", C.c_int64), ("infeasible_kind", C.c_int32), ("infeasible_sum", C.c_double)]
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("dtype", C.c_int), ("device", C.c_int32), ("num_states", C.c_int32), ("num_cols", C.c_int32),
+                ("nnz", C.c_int64), ("stateptr", C.c_void_p), ("colptr", C.c_void_p), ("rowval", C.c_void_p),
+                ("lower", C.c_void_p), ("upper", C.c_void_p)]
+
+
+class GenConfig(C.Structure):
+    _fields_ = [("dtype", C.c_int), ("device", C.c_int32), ("num_states", C.c_int32), ("actions", C.c_int32),
+                ("law", C.c_int32), ("support", C.c_int32), ("alpha", C.c_double), ("kmax", C.c_int32),
+                ("lower_scale", C.c_double), ("upper_scale", C.c_double), ("seed", C.c_uint64),
+                ("state_begin", C.c_int32), ("state_end", C.c_int32)]
+
+
+class ModelInfo(C.Structure):
+    _fields_ = [("dtype", C.c_int), ("device", C.c_int32), ("num_states", C.c_int32), ("num_cols", C.c_int32),
+                ("nnz", C.c_int64), ("state_begin", C.c_int32), ("state_end", C.c_int32),
+                ("max_column_length", C.c_int32), ("num_infeasible_columns", C.c_int32),
+                ("device_bytes", C.c_int64), ("short_columns", C.c_int32), ("mid_columns", C.c_int32),
+                ("long_columns", C.c_int32)]
+
+
+class Plan(C.Structure):
+    _fields_ = [("pessimistic", C.c_int32), ("maximize", C.c_int32), ("finite", C.c_int32), ("horizon", C.c_int64),
+                ("eps", C.c_double), ("max_iterations", C.c_int64), ("initial", C.c_void_p), ("frozen", C.c_void_p),
+                ("rewards", C.c_void_p), ("discount", C.c_double), ("forced", C.c_void_p),
+                ("forced_time_dependent", C.c_int32)]
+
+
+ITER_CB = C.CFUNCTYPE(None, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class Outputs(C.Structure):
+    _fields_ = [("values", C.c_void_p), ("residual", C.c_void_p), ("iterations", C.POINTER(C.c_int64)),
+                ("chosen", C.c_void_p), ("record_all_steps", C.c_int32), ("on_iteration", ITER_CB),
+                ("user", C.c_void_p)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True) -> C.CDLL:
+    """Load the engine library, building it in-tree first if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_build.LIB):
+                if not build_if_missing:
+                    raise FileNotFoundError(f"engine library not built: {_build.LIB}")
+                _build.build()
+            lib = C.CDLL(_build.LIB)
+            lib.rimdp_last_error.restype = C.c_char_p
+            _lib = lib
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != OK:
+        lib = load()
+        info = ErrorInfo()
+        lib.rimdp_last_error_info(C.byref(info))
+        raise EngineError(status, lib.rimdp_last_error().decode(errors="replace"), info)
+
+
+def device_count() -> int:
+    c = C.c_int()
+    _check(load().rimdp_device_count(C.byref(c)))
+    return c.value
+
+
+class RandomSizes(C.Structure):
+    _fields_ = [("num_states", C.c_int32), ("num_cols", C.c_int32), ("nnz", C.c_int64)]
+
+
+def random_imdp(states, actions, density, scale=0.2, seed=1, point=False, dtype=np.float64):
+    """The reference generator's model (random_model.hpp:42-161) as CSC arrays:
+    (stateptr int32, colptr int64, rowval int32, lower, upper)."""
+    lib = load()
+    sz = RandomSizes()
+    h = C.c_void_p()
+    st = lib.rimdp_random_imdp(C.c_int32(states), C.c_int32(actions), C.c_double(density), C.c_double(scale),
+                               C.c_uint64(seed), C.c_int32(int(point)), C.c_int32(_dt(dtype)), C.byref(sz),
+                               C.byref(h))
+    if st:
+        raise ValueError("rimdp_random_imdp: invalid configuration")
+    sp = np.empty(sz.num_states + 1, np.int32)
+    cp = np.empty(sz.num_cols + 1, np.int64)
+    rv = np.empty(sz.nnz, np.int32)
+    lo = np.empty(sz.nnz, dtype)
+    up = np.empty(sz.nnz, dtype)
+    lib.rimdp_random_imdp_take(h, _p(sp), _p(cp), _p(rv), _p(lo), _p(up))
+    return sp, cp, rv, lo, up
+
+
+def _dt(dtype) -> int:
+    return RIMDP_F64 if np.dtype(dtype) == np.float64 else RIMDP_F32
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+class DeviceModel:
+    """A transition store resident in HBM (rimdp_model)."""
+
+    def __init__(self, handle, dtype):
+        self._h = handle
+        self.dtype = np.dtype(dtype)
+        self._keep = []
+        inf = self.info()
+        self.num_states = inf.num_states
+        self.num_cols = inf.num_cols
+        self.nnz = inf.nnz
+        self.state_begin = inf.state_begin
+        self.state_end = inf.state_end
+
+    @classmethod
+    def from_csc(cls, stateptr, colptr, rowval, lower, upper, device: int = 0) -> "DeviceModel":
+        lower = np.asarray(lower)
+        dtype = lower.dtype
+        if dtype not in (np.float64, np.float32):
+            raise TypeError("lower/upper must be float64 or float32")
+        sp = np.ascontiguousarray(stateptr, np.int32)
+        cp = np.ascontiguousarray(colptr, np.int64)
+        rv = np.ascontiguousarray(rowval, np.int32)
+        lo = np.ascontiguousarray(lower, dtype)
+        up = np.ascontiguousarray(upper, dtype)
+        d = ModelDesc(_dt(dtype), device, len(sp) - 1, len(cp) - 1, int(cp[-1]), _p(sp), _p(cp), _p(rv), _p(lo), _p(up))
+        h = C.c_void_p()
+        _check(load().rimdp_model_create(C.byref(d), C.byref(h)))
+        return cls(h, dtype)
+
+    @classmethod
+    def generate(cls, cfg: GenConfig) -> "DeviceModel":
+        h = C.c_void_p()
+        _check(load().rimdp_model_generate(C.byref(cfg), C.byref(h)))
+        return cls(h, np.float64 if cfg.dtype == RIMDP_F64 else np.float32)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().rimdp_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> ModelInfo:
+        i = ModelInfo()
+        _check(load().rimdp_model_info_get(self._h, C.byref(i)))
+        return i
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(load().rimdp_model_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    # -- plans ---------------------------------------------------------------
+    def _plan(self, *, initial, pessimistic=True, maximize=True, finite=True, horizon=0, eps=0.0,
+              max_iterations=1_000_000, frozen=None, rewards=None, discount=0.0, forced=None):
+        keep = []
+        n = self.num_states if self.state_end - self.state_begin == self.num_states else None
+        v0 = np.ascontiguousarray(initial, self.dtype)
+        keep.append(v0)
+        fz = None if frozen is None else np.ascontiguousarray(frozen, np.uint8)
+        rw = None if rewards is None else np.ascontiguousarray(rewards, self.dtype)
+        fc = None if forced is None else np.ascontiguousarray(forced, np.int32)
+        keep += [fz, rw, fc]
+        del n
+        plan = Plan(int(bool(pessimistic)), int(bool(maximize)), int(bool(finite)), int(horizon), float(eps),
+                    int(max_iterations), _p(v0), _p(fz), _p(rw), float(discount), _p(fc),
+                    int(fc is not None and fc.ndim == 2))
+        return plan, keep
+
+    def solve(self, *, record="none", on_iteration=None, **kw):
+        """Full solve.  record: "none" | "last" | "all" (per-step chosen columns)."""
+        plan, keep = self._plan(**kw)
+        nv = len(keep[0])
+        values = np.empty(nv, self.dtype)
+        residual = np.empty(nv, self.dtype)
+        it = C.c_int64()
+        chosen = None
+        if record == "last":
+            chosen = np.empty(self.state_end - self.state_begin, np.int32)
+        elif record == "all":
+            chosen = np.empty((max(int(kw.get("horizon", 0)), 0), self.state_end - self.state_begin), np.int32)
+        cb = ITER_CB()
+        if on_iteration is not None:
+            dt, n = self.dtype, nv
+
+            def _cb(k, vals, user):
+                arr = np.ctypeslib.as_array(C.cast(vals, C.POINTER(C.c_double if dt == np.float64 else C.c_float)),
+                                            shape=(n,)).copy()
+                on_iteration(int(k), arr)
+
+            cb = ITER_CB(_cb)
+        out = Outputs(values.ctypes.data, residual.ctypes.data, C.pointer(it), _p(chosen),
+                      int(record == "all"), cb, None)
+        _check(load().rimdp_solve(self._h, C.byref(plan), C.byref(out)))
+        res = {"values": values, "residual": residual, "iterations": it.value}
+        if chosen is not None:
+            res["chosen"] = chosen
+        return res
+
+    def bellman_step(self, values, pessimistic=True, maximize=True, frozen=None, forced=None):
+        v = np.ascontiguousarray(values, self.dtype)
+        fz = None if frozen is None else np.ascontiguousarray(frozen, np.uint8)
+        fc = None if forced is None else np.ascontiguousarray(forced, np.int32)
+        out = np.empty(len(v), self.dtype)
+        ch = np.empty(self.state_end - self.state_begin, np.int32)
+        _check(load().rimdp_bellman_step(self._h, _p(v), int(bool(pessimistic)), int(bool(maximize)), _p(fz), _p(fc),
+                                         _p(out), _p(ch)))
+        return out, ch
+
+    def column_values(self, values, pessimistic=True):
+        v = np.ascontiguousarray(values, self.dtype)
+        q = np.empty(self.num_cols, self.dtype)
+        _check(load().rimdp_column_values(self._h, _p(v), int(bool(pessimistic)), _p(q)))
+        return q
+
+    # -- split solve (resident benchmarking / sharded driver) ---------------
+    def begin(self, **kw):
+        plan, keep = self._plan(**kw)
+        self._keep = keep
+        _check(load().rimdp_solve_begin(self._h, C.byref(plan)))
+
+    def advance(self, iterations: int):
+        _check(load().rimdp_solve_advance(self._h, C.c_int64(iterations)))
+
+    def poll(self):
+        k, fin, res = C.c_int64(), C.c_int32(), C.c_double()
+        _check(load().rimdp_solve_poll(self._h, C.byref(k), C.byref(fin), C.byref(res)))
+        return k.value, bool(fin.value), res.value
+
+    def finish(self, record=False):
+        nv = len(self._keep[0])
+        values = np.empty(nv, self.dtype)
+        residual = np.empty(nv, self.dtype)
+        it = C.c_int64()
+        out = Outputs(values.ctypes.data, residual.ctypes.data, C.pointer(it), None, 0, ITER_CB(), None)
+        _check(load().rimdp_solve_finish(self._h, C.byref(out)))
+        return {"values": values, "residual": residual, "iterations": it.value}
+
+    def profile(self, on: bool = True):
+        _check(load().rimdp_profile_enable(self._h, int(on)))
+
+    def profile_read(self):
+        """(column-kernel ms, action-kernel ms, iterations, kernels per iteration) since the last read."""
+        c, a, it, kp = C.c_double(), C.c_double(), C.c_int64(), C.c_int32()
+        _check(load().rimdp_profile_read(self._h, C.byref(c), C.byref(a), C.byref(it), C.byref(kp)))
+        return c.value, a.value, it.value, kp.value
+
+    def value_buffers(self):
+        b0, b1 = C.c_void_p(), C.c_void_p()
+        _check(load().rimdp_solve_value_buffers(self._h, C.byref(b0), C.byref(b1)))
+        return b0.value, b1.value
