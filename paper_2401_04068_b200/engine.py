@@ -76,6 +76,41 @@ class Outputs(C.Structure):
 _lib = None
 _lock = threading.Lock()
 
+_VP, _I32, _I64, _D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+_SIGNATURES = {
+    # every entry point of include/rimdp_b200.h and rimdp_b200_workloads.h
+    "rimdp_last_error": ([], C.c_char_p),
+    "rimdp_last_error_info": ([_VP], C.c_int),
+    "rimdp_abi_version": ([], C.c_int),
+    "rimdp_device_count": ([_VP], C.c_int),
+    "rimdp_model_create": ([_VP, _VP], C.c_int),
+    "rimdp_model_destroy": ([_VP], C.c_int),
+    "rimdp_model_generate": ([_VP, _VP], C.c_int),
+    "rimdp_model_read_columns": ([_VP, _I32, _I32, _VP, _VP, _VP, _VP], C.c_int),
+    "rimdp_model_info_get": ([_VP, _VP], C.c_int),
+    "rimdp_model_stream": ([_VP, _VP], C.c_int),
+    "rimdp_solve": ([_VP, _VP, _VP], C.c_int),
+    "rimdp_solve_begin": ([_VP, _VP], C.c_int),
+    "rimdp_solve_advance": ([_VP, _I64], C.c_int),
+    "rimdp_solve_poll": ([_VP, _VP, _VP, _VP], C.c_int),
+    "rimdp_solve_finish": ([_VP, _VP], C.c_int),
+    "rimdp_solve_value_buffers": ([_VP, _VP, _VP], C.c_int),
+    "rimdp_profile_enable": ([_VP, _I32], C.c_int),
+    "rimdp_profile_read": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
+    "rimdp_bellman_step": ([_VP, _VP, _I32, _I32, _VP, _VP, _VP, _VP], C.c_int),
+    "rimdp_column_values": ([_VP, _VP, _I32, _VP], C.c_int),
+    "rimdp_random_imdp": ([_I32, _I32, _D, _D, C.c_uint64, _I32, _I32, _VP, _VP], C.c_int),
+    "rimdp_random_imdp_take": ([_VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
+}
+
+
+def _declare(lib) -> None:
+    """Full prototypes: pointers must never be narrowed to C int."""
+    for name, (args, res) in _SIGNATURES.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+
 
 def library_path() -> str:
     return _build.LIB
@@ -91,7 +126,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
                     raise FileNotFoundError(f"engine library not built: {_build.LIB}")
                 _build.build()
             lib = C.CDLL(_build.LIB)
-            lib.rimdp_last_error.restype = C.c_char_p
+            _declare(lib)
             _lib = lib
     return _lib
 
