@@ -82,7 +82,7 @@ struct Infeasible {
 };
 
 struct SolveState {
-    DevBuf v[2], q, chosen, frozen, rewards, forced, res, ctl;
+    DevBuf v[2], q, chosen, frozen, rewards, forced, res, ctl, work;
     bool has_frozen = false, has_rewards = false, has_forced = false;
     int forced_td = 0;
     int pess = 1, maxi = 1, finite = 1;
@@ -277,18 +277,20 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     }
     Ctl c{};
     CK(cudaMemcpyAsync(s.ctl.p, &c, sizeof c, cudaMemcpyHostToDevice, m->stream));
+    s.work.ensure(2 * sizeof(unsigned));
+    CK(cudaMemsetAsync(s.work.p, 0, 2 * sizeof(unsigned), m->stream));
     s.launched = 0;
     s.active = true;
 }
 
 template <class T>
-void launch_columns(rimdp_model* m, const T* V, T* q, Ctl* ctl, bool pess) {
+void launch_columns(rimdp_model* m, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
     if (m->nshort > 0) {
-        const int blocks = grid_for(m->nshort, kShortBatch * kWarpsPerBlock, m->sm_count, 6);
+        const int blocks = grid_for(m->nshort, kShortBatch * kWarpsPerBlock, m->sm_count, 5);
         auto k = pess ? omax_short<T, true> : omax_short<T, false>;
         k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(m->nshort, m->short_list.as<int>(), m->colptr.as<long long>(),
                                                           m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
-                                                          m->rem.as<T>(), V, q, ctl);
+                                                          m->rem.as<T>(), V, q, ctl, work);
     }
     if (m->nlong > 0) {
         const int blocks = grid_for(m->nlong, kWarpsPerBlock, m->sm_count, 8);
@@ -316,7 +318,7 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
         s.events_used += 3;
         CK(cudaEventRecord(ev[0], m->stream));
     }
-    launch_columns<T>(m, vin, s.q.as<T>(), ctl, s.pess);
+    launch_columns<T>(m, vin, s.q.as<T>(), ctl, s.pess, s.work.as<unsigned>() + (k & 1));
     if (ev) CK(cudaEventRecord(ev[1], m->stream));
     ActionArgs a{};
     a.n = m->n;
@@ -333,6 +335,7 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     a.max_iterations = s.max_iterations;
     a.k = k;
     a.record_only = s.record_only;
+    a.work = s.work.as<unsigned>();
     action_reduce<T><<<grid_for(m->n, 256, m->sm_count, 8), 256, 0, m->stream>>>(
         a, s.q.as<T>(), vin, vout, s.has_rewards ? s.rewards.as<T>() : nullptr, (T)s.discount, (T)s.eps, ctl);
     if (ev) CK(cudaEventRecord(ev[2], m->stream));
@@ -537,7 +540,9 @@ int column_values_t(rimdp_model* m, const void* v_in, int pess, void* q_out) {
     s.v[0].ensure(sizeof(T) * m->n_global);
     s.q.ensure(sizeof(T) * std::max(1, m->ncols));
     CK(cudaMemcpyAsync(s.v[0].p, v_in, sizeof(T) * m->n_global, cudaMemcpyHostToDevice, m->stream));
-    launch_columns<T>(m, s.v[0].as<T>(), s.q.as<T>(), nullptr, pess != 0);
+    s.work.ensure(2 * sizeof(unsigned));
+    CK(cudaMemsetAsync(s.work.p, 0, 2 * sizeof(unsigned), m->stream));
+    launch_columns<T>(m, s.v[0].as<T>(), s.q.as<T>(), nullptr, pess != 0, s.work.as<unsigned>());
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(q_out, s.q.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));

@@ -22,6 +22,8 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstring>
+#include <type_traits>
 
 namespace rimdp_dev {
 
@@ -133,72 +135,169 @@ __device__ __forceinline__ bool warp_argmin_pos(Bits key, int pos, bool active, 
 }
 
 // ---------------------------------------------------------------------------
-// Short columns (<= 32 entries).  A warp takes 16 columns at a time.  For
-// each column, lane i owns entry i: coalesced loads, one V gather, and the
-// greedy assignment driven by exact warp argmins (one per position that
-// receives mass; typically 1-3).  Products V[row_i] * p_i go to shared
-// memory; then lane t sums column t's products sequentially in row order.
+// Short columns (<= 32 entries).
+//
+// A warp walks a stream of columns in batches of 16 (the first batch per
+// warp static, the rest handed out by an atomic work counter).  For each column, lane i owns entry i: coalesced loads of
+// (row, lower, gap), one V gather, and the greedy assignment driven by exact
+// warp argmins — one per position that receives extra mass (1-3 on typical
+// models).  Products V[row_i] * p_i are staged in shared memory; at the end
+// of a batch lane t sums column t's products sequentially in row order.
+//
+// Latency: the row -> V gather is a dependent pair of memory round trips, so
+// the kernel is software-pipelined three deep — while column i is reduced,
+// (lower, gap, V[row]) of column i+1 and the rows of column i+2 are in
+// flight.  Column metadata (start, length, rem) lives in a 32-lane window:
+// lanes 0-15 hold the current batch, lanes 16-31 the next one, prefetched a
+// whole batch ahead.
+template <class T>
+__device__ __forceinline__ typename Num<T>::Bits order_key(T v, bool pess) {
+    using Bits = typename Num<T>::Bits;
+    using SBits = typename std::conditional<sizeof(T) == 8, long long, int>::type;
+    constexpr Bits kMsb = Bits(1) << (8 * sizeof(Bits) - 1);
+    Bits b;
+    const T z = Num<T>::add(v, T(0)); // -0 -> +0: the reference orders with != (ties by row)
+    memcpy(&b, &z, sizeof b);
+    const Bits s = static_cast<Bits>(static_cast<SBits>(b) >> (8 * sizeof(Bits) - 1));
+    return pess ? (b ^ (s | kMsb)) : (b ^ (~s & ~kMsb));
+}
+
+// Lane with the smallest (key, lane); inactive lanes carry the all-ones key.
+template <class Bits>
+__device__ __forceinline__ int warp_argmin_sentinel(Bits key) {
+    if constexpr (sizeof(Bits) == 8) {
+        const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+        const unsigned mhi = __reduce_min_sync(kFull, hi);
+        const unsigned mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xffffffffu);
+        return __ffs(__ballot_sync(kFull, hi == mhi && lo == mlo)) - 1;
+    } else {
+        const unsigned mk = __reduce_min_sync(kFull, static_cast<unsigned>(key));
+        return __ffs(__ballot_sync(kFull, static_cast<unsigned>(key) == mk)) - 1;
+    }
+}
+
 template <class T, bool kPess>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 5)
 omax_short(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
            const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
-           const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl) {
+           const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl,
+           unsigned* __restrict__ work) {
     using N = Num<T>;
     using Bits = typename N::Bits;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     __shared__ T xs[kWarpsPerBlock][kShortBatch][kShortLen + 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
-    for (int base = gw * kShortBatch; base < nlist; base += nw * kShortBatch) {
-        const int mine = base + (lane & (kShortBatch - 1));
-        int c = -1;
-        long long beg = 0;
-        int len = 0;
-        T crem = T(0);
-        if (lane < kShortBatch && mine < nlist) {
-            c = list[mine];
-            beg = colptr[c];
-            len = static_cast<int>(colptr[c + 1] - beg);
-            crem = rem[c];
+    // batches: the first one static, the rest handed out by a work counter
+    auto next_batch = [&]() -> int {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(work, 1u);
+        return nw + static_cast<int>(__shfl_sync(kFull, t, 0));
+    };
+    int base = gw * kShortBatch;
+    if (base >= nlist) return;
+    int nbase = next_batch() * kShortBatch;
+
+    // metadata window: lane j describes column j of [current batch | next batch]
+    int mc = -1, mlen = 0;
+    long long mbeg = 0;
+    T mrem = T(0);
+    auto load_meta = [&](int batch_base) {
+        const int idx = batch_base + (lane & (kShortBatch - 1));
+        mc = -1;
+        mlen = 0;
+        mbeg = 0;
+        mrem = T(0);
+        if (batch_base < nlist && idx < nlist) {
+            mc = __ldg(list + idx);
+            mbeg = __ldg(colptr + mc);
+            mlen = static_cast<int>(__ldg(colptr + mc + 1) - mbeg);
+            mrem = __ldg(rem + mc);
         }
-        const int ncol = min(kShortBatch, nlist - base);
-        for (int k = 0; k < ncol; ++k) {
-            const long long b = __shfl_sync(kFull, beg, k);
-            const int L = __shfl_sync(kFull, len, k);
-            const T r = __shfl_sync(kFull, crem, k);
-            const bool valid = lane < L;
-            T l = T(0), g = T(0), v = T(0);
-            if (valid) {
-                const int row = __ldg(rows + b + lane);
-                l = __ldg(lower + b + lane);
-                g = __ldg(gap + b + lane);
-                v = __ldg(V + row);
+    };
+    load_meta(lane < kShortBatch ? base : nbase);
+
+    // pipeline prologue: data of column 0, rows of column 1
+    long long bn = __shfl_sync(kFull, mbeg, 0), bnn = __shfl_sync(kFull, mbeg, 1);
+    int Ln = __shfl_sync(kFull, mlen, 0), Lnn = __shfl_sync(kFull, mlen, 1);
+    int rowA = lane < Ln ? __ldg(rows + bn + lane) : 0;
+    T lc = T(0), gc = T(0), vc = T(0);
+    int Lc = Ln;
+    if (lane < Ln) {
+        lc = __ldg(lower + bn + lane);
+        gc = __ldg(gap + bn + lane);
+        vc = __ldg(V + rowA);
+    }
+    bn = bnn;
+    Ln = Lnn;
+    rowA = lane < Ln ? __ldg(rows + bn + lane) : 0;
+    bnn = __shfl_sync(kFull, mbeg, 2);
+    Lnn = __shfl_sync(kFull, mlen, 2);
+
+    for (;;) {
+        for (int s = 0; s < kShortBatch; ++s) {
+            // stage D: (lower, gap, V[row]) of column i+1
+            T ln = T(0), gn = T(0), vn = T(0);
+            if (lane < Ln) {
+                ln = __ldg(lower + bn + lane);
+                gn = __ldg(gap + bn + lane);
+                vn = __ldg(V + rowA);
             }
-            T p = l;
-            const Bits key = N::key(v, kPess);
-            bool active = valid;
+            // stage R: rows of column i+2
+            const int rowB = lane < Lnn ? __ldg(rows + bnn + lane) : 0;
+            // stage C: the greedy O-max of column i (omax.hpp:98-112)
+            const T r = __shfl_sync(kFull, mrem, s);
+            const bool valid = lane < Lc;
+            Bits key = valid ? order_key<T>(vc, kPess) : ~Bits(0);
+            T p = lc;
             T consumed = T(0);
-            for (;;) {
-                const T avail = N::sub(r, consumed);
-                if (!(avail > T(0))) break;
-                const int sel = warp_argmin_lane(key, active);
-                if (sel < 0) break;
-                const T gs = __shfl_sync(kFull, g, sel);
+            T avail = r;
+            for (int nsel = 0; avail > T(0) && nsel < Lc; ++nsel) {
+                const int sel = warp_argmin_sentinel(key);
+                const T gs = __shfl_sync(kFull, gc, sel);
                 if (lane == sel) {
-                    p = N::add(l, g < avail ? g : avail);
-                    active = false;
+                    p = N::add(lc, gc < avail ? gc : avail);
+                    key = ~Bits(0);
                 }
                 consumed = N::add(consumed, gs);
+                avail = N::sub(r, consumed);
             }
-            if (valid) xs[w][k][lane] = N::mul(v, p);
+            if (valid) xs[w][s][lane] = N::mul(vc, p);
+            // rotate the pipeline; metadata of column i+3 = window lane s+3
+            lc = ln;
+            gc = gn;
+            vc = vn;
+            Lc = Ln;
+            rowA = rowB;
+            bn = bnn;
+            Ln = Lnn;
+            bnn = __shfl_sync(kFull, mbeg, s + 3);
+            Lnn = __shfl_sync(kFull, mlen, s + 3);
         }
+        // row-order expectation of the batch's columns (omax.hpp:169-173)
         __syncwarp();
-        if (c >= 0) {
+        if (lane < kShortBatch && mc >= 0) {
             T acc = T(0);
-            for (int i = 0; i < len; ++i) acc = N::add(acc, xs[w][lane][i]);
-            q[c] = acc;
+            for (int i = 0; i < mlen; ++i) acc = N::add(acc, xs[w][lane][i]);
+            q[mc] = acc;
         }
         __syncwarp();
+        base = nbase;
+        if (base >= nlist) break;
+        nbase = next_batch() * kShortBatch;
+        // shift the window and prefetch the batch after next
+        const int c2 = __shfl_down_sync(kFull, mc, kShortBatch);
+        const long long b2 = __shfl_down_sync(kFull, mbeg, kShortBatch);
+        const int l2 = __shfl_down_sync(kFull, mlen, kShortBatch);
+        const T r2 = __shfl_down_sync(kFull, mrem, kShortBatch);
+        if (lane < kShortBatch) {
+            mc = c2;
+            mbeg = b2;
+            mlen = l2;
+            mrem = r2;
+        } else {
+            load_meta(nbase);
+        }
     }
 }
 
@@ -317,6 +416,7 @@ struct ActionArgs {
     long long max_iterations;
     long long k;                   // the iteration this launch computes (1-based)
     int record_only;               // sharded solves: the driver owns the stop test
+    unsigned* work;                // column-kernel work counters, slot k & 1
 };
 
 template <class T>
@@ -381,6 +481,7 @@ action_reduce(ActionArgs a, const T* __restrict__ q, const T* __restrict__ vin, 
         ctl->k = a.k;
         ctl->res_last = static_cast<double>(res);
         ctl->res_bits[(a.k + 1) & 1] = 0ull;
+        if (a.work) a.work[(a.k + 1) & 1] = 0u;
         ctl->arrive = 0u;
         if (a.record_only) {
             // global residual is reduced across ranks by the sharded driver
