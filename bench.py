@@ -55,7 +55,10 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons, sampled every 20 ms from before the
+    timed region until after the last GPU phase (timed region, kernel-timing
+    pass and the end-to-end solve): every sample after the "timed" mark is
+    taken under load."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -64,11 +67,12 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        self.marks = {}
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -78,7 +82,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, name):
+        self.marks[name] = time.perf_counter()
 
     def __exit__(self, *exc):
         if self.proc:
@@ -87,24 +94,29 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+            self.proc = None
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        t0 = self.marks.get("timed", 0.0)
+        t1 = self.marks.get("end", float("inf"))
+        sm, mx, reasons, inside = [], None, set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 6 or ts < t0:
                 continue
             try:
                 sm.append(float(parts[0]))
                 mx = float(parts[1])
             except ValueError:
                 continue
+            inside += ts <= t1 + 0.02
             for nm, v in zip(names, parts[2:]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "samples_in_timed_region": inside,
+                "window": "timed region through kernel-timing pass and end-to-end solve (GPU busy)"}
 
 
 def make_problem(w):
@@ -142,6 +154,8 @@ def engine_arm(args, w):
     total = args.warmup + args.steps
     kw = dict(initial=plan.initial, frozen=plan.frozen, finite=True, horizon=total + 1,
               pessimistic=w["pessimistic"], maximize=w["maximize"])
+    clk = ClockSampler(local).__enter__()  # sampled through every GPU phase below
+    time.sleep(0.3)  # let nvidia-smi start sampling before the GPU work begins
     m.begin(**kw)
     m.advance(args.warmup)
     m.poll()
@@ -149,11 +163,12 @@ def engine_arm(args, w):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        start.record(stream)
-        m.advance(args.steps)
-        end.record(stream)
-        torch.cuda.synchronize()
+    clk.mark("timed")
+    start.record(stream)
+    m.advance(args.steps)
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk.mark("end")
     ms = start.elapsed_time(end)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -171,15 +186,18 @@ def engine_arm(args, w):
     m.profile_read()
     prof_iters = min(args.steps, 200)
     m.advance(prof_iters)
-    col_ms, act_ms, it, kpi = m.profile_read()
+    fused_ms, cols_ms, act_ms, it, kpi = m.profile_read()
     m.profile(False)
     m.finish()
-    col_avg = col_ms / it
-    act_avg = act_ms / it
+    fused_avg, cols_avg, act_avg = fused_ms / it, cols_ms / it, act_ms / it
+    if fused_avg >= cols_avg:
+        kernel_name, kernel_avg = "bellman_short (fused column O-max + action + residual)", fused_avg
+    else:
+        kernel_name, kernel_avg = "omax_long/omax_short (per-column O-max of long states)", cols_avg
     es = 8
     alg_bytes = nnz * (4 + es + es + es)  # index + lower + gap + V gather
     peak, peak_src = load_peaks()
-    achieved = alg_bytes / (col_avg * 1e-3) / 1e9
+    achieved = alg_bytes / (kernel_avg * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
@@ -210,6 +228,7 @@ def engine_arm(args, w):
             bit_exact = (hashlib.sha256(vf.values.tobytes()).hexdigest() == run["values_sha256"] and
                          hashlib.sha256(vf.residual.tobytes()).hexdigest() == run["residual_sha256"])
 
+    clk.__exit__()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample(arrays, w, plan, budget_s=args.cpu_budget)
@@ -233,9 +252,11 @@ def engine_arm(args, w):
                    "l2": "per-iteration inputs (28 B x transitions) exceed the 126 MB L2; no flush needed",
                    "scheduler": {"short_columns": info.short_columns, "long_columns": info.long_columns}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "omax_short (column O-max)",
-                     "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": col_avg,
-                     "action_kernel_ms": act_avg, "column_share_of_step": col_avg / (col_avg + act_avg),
+                     "traffic": traffic, "kernel": kernel_name,
+                     "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": kernel_avg,
+                     "phase_ms": {"fused_short_states": fused_avg, "column_kernels": cols_avg,
+                                  "action_kernel": act_avg},
+                     "kernel_share_of_step": kernel_avg / max(fused_avg + cols_avg + act_avg, 1e-12),
                      "peak_source": peak_src},
         "e2e": {"value": nnz * e2e_iters / e2e_s, "unit": "transitions/s", "h2d_bytes_per_step": h2d / e2e_iters,
                 "d2h_bytes_per_step": d2h / e2e_iters, "seconds_to_convergence": e2e_s, "iterations": e2e_iters,

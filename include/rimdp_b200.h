@@ -175,12 +175,13 @@ int rimdp_solve_poll(rimdp_model* model, int64_t* iterations_done, int32_t* fini
 int rimdp_solve_finish(rimdp_model* model, const rimdp_outputs* out);
 
 /* Kernel timing: when enabled, every enqueued iteration records CUDA events
- * on the model stream around its column kernels and its action kernel.
- * profile_read synchronises, returns the summed milliseconds and the
- * iteration count since the last read, and resets the accumulators. */
+ * on the model stream around its three phases: the fused short-state kernel,
+ * the per-column kernels of the remaining states, and their action kernel.
+ * profile_read synchronises, returns the summed milliseconds of each phase
+ * and the iteration count since the last read, and resets the accumulators. */
 int rimdp_profile_enable(rimdp_model* model, int32_t on);
-int rimdp_profile_read(rimdp_model* model, double* column_ms, double* action_ms, int64_t* iterations,
-                       int32_t* kernels_per_iteration);
+int rimdp_profile_read(rimdp_model* model, double* fused_ms, double* columns_ms, double* action_ms,
+                       int64_t* iterations, int32_t* kernels_per_iteration);
 
 /* Device pointers of the solve's double-buffered value vector, for
  * collective exchange in the sharded driver: V_k lives in buffer k & 1. */

@@ -115,7 +115,10 @@ struct rimdp_model {
     long long nnz = 0;
     int maxlen = 0;
     DevBuf stateptr, colptr, rows, lower, gap, rem, infeasible, quoted, short_list, long_list, scratch;
-    int nshort = 0, nlong = 0;
+    DevBuf q_short_list, q_long_list, batch_slots, batch_states, long_states;
+    int nshort = 0, nlong = 0;                // all columns by length (column_values)
+    int nq_short = 0, nq_long = 0;            // columns of long states (q path)
+    int nbatch = 0, nlong_states = 0;         // fused short-state batches / q-path states
     std::vector<int> h_stateptr;
     std::vector<Infeasible> infeasible_cols;
     long long device_bytes = 0;
@@ -155,25 +158,77 @@ int grid_for(long long work, int per_block, int sm_count, int blocks_per_sm) {
     return (int)std::max<long long>(g, 1);
 }
 
-// Column scheduler: route each column by length.
+template <class U>
+void upload_list(rimdp_model* m, DevBuf& buf, const std::vector<U>& v) {
+    buf.ensure(sizeof(U) * std::max<size_t>(1, v.size()));
+    if (!v.empty()) CK(cudaMemcpyAsync(buf.p, v.data(), sizeof(U) * v.size(), cudaMemcpyHostToDevice, m->stream));
+}
+
+// Column scheduler:
+//  * every column is routed by length: <= 32 entries -> warp-per-column
+//    lane-per-entry kernel, longer -> warp-per-column strided kernel
+//    (these lists serve rimdp_column_values);
+//  * for iterations, runs of consecutive "short states" (<= 16 columns, all
+//    columns <= 32 entries) are packed into state-aligned batches of <= 16
+//    column slots for the fused bellman_short kernel; the remaining "long
+//    states" take the q path (column kernels + action_reduce).
 void build_schedule(rimdp_model* m, const long long* h_colptr) {
-    std::vector<int> shortl, longl;
-    shortl.reserve(m->ncols);
+    std::vector<int> cs, cl, qs, ql, slots, lstates;
+    std::vector<int2> bstates;
+    cs.reserve(m->ncols);
     int maxlen = 0;
     for (int c = 0; c < m->ncols; ++c) {
         const long long len = h_colptr[c + 1] - h_colptr[c];
-        maxlen = std::max<long long>(maxlen, len);
-        (len <= kShortLen ? shortl : longl).push_back(c);
+        maxlen = (int)std::max<long long>(maxlen, len);
+        (len <= kShortLen ? cs : cl).push_back(c);
     }
+    const std::vector<int>& sp = m->h_stateptr;
+    auto short_state = [&](int s) {
+        const int na = sp[s + 1] - sp[s];
+        if (na < 1 || na > kShortBatch) return false;
+        for (int c = sp[s]; c < sp[s + 1]; ++c)
+            if (h_colptr[c + 1] - h_colptr[c] > kShortLen) return false;
+        return true;
+    };
+    int s0 = -1, used = 0;
+    auto close_batch = [&]() {
+        if (s0 < 0) return;
+        for (int j = used; j < kShortBatch; ++j) slots.push_back(-1);
+        s0 = -1;
+        used = 0;
+    };
+    for (int s = 0; s < m->n; ++s) {
+        if (!short_state(s)) {
+            close_batch();
+            lstates.push_back(s);
+            for (int c = sp[s]; c < sp[s + 1]; ++c) (h_colptr[c + 1] - h_colptr[c] <= kShortLen ? qs : ql).push_back(c);
+            continue;
+        }
+        const int na = sp[s + 1] - sp[s];
+        if (s0 >= 0 && (used + na > kShortBatch || s - s0 >= kShortBatch)) close_batch();
+        if (s0 < 0) {
+            s0 = s;
+            bstates.push_back(make_int2(s, 0));
+        }
+        for (int c = sp[s]; c < sp[s + 1]; ++c) slots.push_back(c);
+        used += na;
+        bstates.back().y += 1;
+    }
+    close_batch();
     m->maxlen = maxlen;
-    m->nshort = (int)shortl.size();
-    m->nlong = (int)longl.size();
-    m->short_list.ensure(sizeof(int) * std::max<size_t>(1, shortl.size()));
-    m->long_list.ensure(sizeof(int) * std::max<size_t>(1, longl.size()));
-    if (!shortl.empty())
-        CK(cudaMemcpyAsync(m->short_list.p, shortl.data(), sizeof(int) * shortl.size(), cudaMemcpyHostToDevice, m->stream));
-    if (!longl.empty())
-        CK(cudaMemcpyAsync(m->long_list.p, longl.data(), sizeof(int) * longl.size(), cudaMemcpyHostToDevice, m->stream));
+    m->nshort = (int)cs.size();
+    m->nlong = (int)cl.size();
+    m->nq_short = (int)qs.size();
+    m->nq_long = (int)ql.size();
+    m->nbatch = (int)bstates.size();
+    m->nlong_states = (int)lstates.size();
+    upload_list(m, m->short_list, cs);
+    upload_list(m, m->long_list, cl);
+    upload_list(m, m->q_short_list, qs);
+    upload_list(m, m->q_long_list, ql);
+    upload_list(m, m->batch_slots, slots);
+    upload_list(m, m->batch_states, bstates);
+    upload_list(m, m->long_states, lstates);
     CK(cudaStreamSynchronize(m->stream));
 }
 
@@ -277,49 +332,52 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     }
     Ctl c{};
     CK(cudaMemcpyAsync(s.ctl.p, &c, sizeof c, cudaMemcpyHostToDevice, m->stream));
-    s.work.ensure(2 * sizeof(unsigned));
-    CK(cudaMemsetAsync(s.work.p, 0, 2 * sizeof(unsigned), m->stream));
+    s.work.ensure(2 * kWorkKinds * sizeof(unsigned));
+    CK(cudaMemsetAsync(s.work.p, 0, 2 * kWorkKinds * sizeof(unsigned), m->stream));
     s.launched = 0;
     s.active = true;
 }
 
+// Per-column expectations q for the columns in the two length-routed lists.
 template <class T>
-void launch_columns(rimdp_model* m, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
-    if (m->nshort > 0) {
-        const int blocks = grid_for(m->nshort, kShortBatch * kWarpsPerBlock, m->sm_count, 5);
+void launch_columns(rimdp_model* m, int ns, const DevBuf& sl, int nl, const DevBuf& ll, const T* V, T* q, Ctl* ctl,
+                    bool pess, unsigned* work) {
+    if (ns > 0) {
+        const int blocks = grid_for(ns, kShortBatch * kWarpsPerBlock, m->sm_count, 5);
         auto k = pess ? omax_short<T, true> : omax_short<T, false>;
-        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(m->nshort, m->short_list.as<int>(), m->colptr.as<long long>(),
-                                                          m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
-                                                          m->rem.as<T>(), V, q, ctl, work);
+        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(ns, sl.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+                                                          m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl,
+                                                          work);
     }
-    if (m->nlong > 0) {
-        const int blocks = grid_for(m->nlong, kWarpsPerBlock, m->sm_count, 8);
+    if (nl > 0) {
+        const int blocks = grid_for(nl, kWarpsPerBlock, m->sm_count, 8);
         auto k = pess ? omax_long<T, true> : omax_long<T, false>;
-        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(m->nlong, m->long_list.as<int>(), m->colptr.as<long long>(),
-                                                         m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
-                                                         m->rem.as<T>(), V, q, ctl);
+        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(nl, ll.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+                                                         m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
     }
 }
 
+// One Bellman iteration: [q path for long states: column kernels] ->
+// [fused bellman_short over the short-state batches] -> [action_reduce over
+// the long states].  The last launch of the three runs the stop test.
 template <class T>
 void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     SolveState& s = m->s;
     const T* vin = s.v[(k - 1) & 1].as<T>();
     T* vout = s.v[k & 1].as<T>();
     Ctl* ctl = s.ctl.as<Ctl>();
+    unsigned* work = s.work.as<unsigned>() + (k & 1) * kWorkKinds;
     cudaEvent_t* ev = nullptr;
     if (s.profile) {
-        while (s.events.size() < s.events_used + 3) {
+        while (s.events.size() < s.events_used + 4) {
             cudaEvent_t e;
             CK(cudaEventCreate(&e));
             s.events.push_back(e);
         }
         ev = &s.events[s.events_used];
-        s.events_used += 3;
+        s.events_used += 4;
         CK(cudaEventRecord(ev[0], m->stream));
     }
-    launch_columns<T>(m, vin, s.q.as<T>(), ctl, s.pess, s.work.as<unsigned>() + (k & 1));
-    if (ev) CK(cudaEventRecord(ev[1], m->stream));
     ActionArgs a{};
     a.n = m->n;
     a.state_begin = m->state_begin;
@@ -336,13 +394,32 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     a.k = k;
     a.record_only = s.record_only;
     a.work = s.work.as<unsigned>();
-    action_reduce<T><<<grid_for(m->n, 256, m->sm_count, 8), 256, 0, m->stream>>>(
-        a, s.q.as<T>(), vin, vout, s.has_rewards ? s.rewards.as<T>() : nullptr, (T)s.discount, (T)s.eps, ctl);
+    const T* rw = s.has_rewards ? s.rewards.as<T>() : nullptr;
+    if (m->nbatch > 0) {
+        a.finalize = m->nlong_states == 0;
+        const int blocks = grid_for((long long)m->nbatch, kWarpsPerBlock, m->sm_count, kShortBlocksPerSm);
+        auto kern = s.pess ? bellman_short<T, true> : bellman_short<T, false>;
+        kern<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(
+            m->nbatch, m->batch_slots.as<int>(), m->batch_states.as<int2>(), m->colptr.as<long long>(),
+            m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), vin, vout, rw, (T)s.discount,
+            (T)s.eps, a, ctl);
+    }
+    if (ev) CK(cudaEventRecord(ev[1], m->stream));
+    launch_columns<T>(m, m->nq_short, m->q_short_list, m->nq_long, m->q_long_list, vin, s.q.as<T>(), ctl, s.pess,
+                      work);
     if (ev) CK(cudaEventRecord(ev[2], m->stream));
+    if (m->nlong_states > 0) {
+        a.finalize = 1;
+        action_reduce<T><<<grid_for(m->nlong_states, 256, m->sm_count, 8), 256, 0, m->stream>>>(
+            a, m->nlong_states, m->long_states.as<int>(), s.q.as<T>(), vin, vout, rw, (T)s.discount, (T)s.eps, ctl);
+    }
+    if (ev) CK(cudaEventRecord(ev[3], m->stream));
     CK(cudaGetLastError());
 }
 
-int kernels_per_iteration(const rimdp_model* m) { return (m->nshort > 0) + (m->nlong > 0) + 1; }
+int kernels_per_iteration(const rimdp_model* m) {
+    return (m->nbatch > 0) + (m->nq_short > 0) + (m->nq_long > 0) + (m->nlong_states > 0);
+}
 
 // First infeasible column that a step would evaluate (bellman.hpp:88-112:
 // frozen states are skipped, forced states evaluate one column; the lowest
@@ -540,9 +617,10 @@ int column_values_t(rimdp_model* m, const void* v_in, int pess, void* q_out) {
     s.v[0].ensure(sizeof(T) * m->n_global);
     s.q.ensure(sizeof(T) * std::max(1, m->ncols));
     CK(cudaMemcpyAsync(s.v[0].p, v_in, sizeof(T) * m->n_global, cudaMemcpyHostToDevice, m->stream));
-    s.work.ensure(2 * sizeof(unsigned));
-    CK(cudaMemsetAsync(s.work.p, 0, 2 * sizeof(unsigned), m->stream));
-    launch_columns<T>(m, s.v[0].as<T>(), s.q.as<T>(), nullptr, pess != 0, s.work.as<unsigned>());
+    s.work.ensure(2 * kWorkKinds * sizeof(unsigned));
+    CK(cudaMemsetAsync(s.work.p, 0, 2 * kWorkKinds * sizeof(unsigned), m->stream));
+    launch_columns<T>(m, m->nshort, m->short_list, m->nlong, m->long_list, s.v[0].as<T>(), s.q.as<T>(), nullptr,
+                      pess != 0, s.work.as<unsigned>());
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(q_out, s.q.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
@@ -748,24 +826,27 @@ int rimdp_profile_enable(rimdp_model* m, int32_t on) {
     return RIMDP_OK;
 }
 
-int rimdp_profile_read(rimdp_model* m, double* column_ms, double* action_ms, int64_t* iterations,
+int rimdp_profile_read(rimdp_model* m, double* fused_ms, double* columns_ms, double* action_ms, int64_t* iterations,
                        int32_t* kernels) {
     if (!m) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null model");
     return guarded([&]() -> int {
         DeviceGuard g(m->device);
         CK(cudaStreamSynchronize(m->stream));
-        double c = 0, a = 0;
+        double f = 0, c = 0, a = 0;
         long long it = 0;
-        for (size_t i = 0; i + 3 <= m->s.events_used; i += 3) {
-            float x = 0, y = 0;
+        for (size_t i = 0; i + 4 <= m->s.events_used; i += 4) {
+            float x = 0, y = 0, z = 0;
             CK(cudaEventElapsedTime(&x, m->s.events[i], m->s.events[i + 1]));
             CK(cudaEventElapsedTime(&y, m->s.events[i + 1], m->s.events[i + 2]));
-            c += x;
-            a += y;
+            CK(cudaEventElapsedTime(&z, m->s.events[i + 2], m->s.events[i + 3]));
+            f += x;
+            c += y;
+            a += z;
             ++it;
         }
         m->s.events_used = 0;
-        if (column_ms) *column_ms = c;
+        if (fused_ms) *fused_ms = f;
+        if (columns_ms) *columns_ms = c;
         if (action_ms) *action_ms = a;
         if (iterations) *iterations = it;
         if (kernels) *kernels = kernels_per_iteration(m);

@@ -32,6 +32,10 @@ constexpr int kShortLen = 32;        // columns with <= 32 entries: one lane per
 constexpr int kShortBatch = 16;      // columns per warp batch in the short kernel
 constexpr int kWarpsPerBlock = 8;
 constexpr int kMaxPartial = 4;       // partially-filled positions tracked per long column
+#ifndef RIMDP_SHORT_BLOCKS_PER_SM
+#define RIMDP_SHORT_BLOCKS_PER_SM 4
+#endif
+constexpr int kShortBlocksPerSm = RIMDP_SHORT_BLOCKS_PER_SM; // resident blocks of bellman_short
 
 // Device loop state of one solve.
 struct Ctl {
@@ -363,7 +367,7 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
             lastk = mk;
             lastp = mp;
         }
-        if (npart > kMaxPartial && lane == 0) atomicExch(&ctl->status, 2);
+        if (npart > kMaxPartial && lane == 0 && ctl) atomicExch(&ctl->status, 2);
         // expectation in row order
         T acc = T(0);
         for (int j0 = 0; j0 < L; j0 += 32) {
@@ -396,13 +400,14 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// Action reduction + reach/avoid/discount update + residual + stop test, one
-// thread per state (bellman.hpp:88-115, solver.hpp:107-134).  The block max
-// of |V_k - V_{k-1}| is folded with one atomicMax; the last block to finish
-// evaluates the stop test for iteration k, so the residual needs no extra
-// pass and the host needs no per-iteration synchronisation.
+// Action reduction + reach/avoid/discount update + residual + stop test
+// (bellman.hpp:88-115, solver.hpp:107-134).  Each block folds its max of
+// |V_k - V_{k-1}| into ctl with one atomicMax; the launch flagged `finalize`
+// (the last kernel of the iteration) counts block arrivals and its last block
+// evaluates the stop test, so the residual needs no extra pass and the host
+// needs no per-iteration synchronisation.
 struct ActionArgs {
-    int n;
+    int n;                         // local states
     int state_begin;               // shard offset of local state 0 in the global value vector
     const int* stateptr;           // local columns of local states
     const unsigned char* frozen;   // local [n] or null
@@ -416,19 +421,81 @@ struct ActionArgs {
     long long max_iterations;
     long long k;                   // the iteration this launch computes (1-based)
     int record_only;               // sharded solves: the driver owns the stop test
-    unsigned* work;                // column-kernel work counters, slot k & 1
+    int finalize;                  // this launch is the iteration's last: run the stop test
+    unsigned* work;                // work counters [2 slots][kWorkKinds], slot k & 1
 };
 
+constexpr int kWorkKinds = 4;      // 0: omax_short (q path), 1: bellman_short, 2: omax_long
+
+__device__ __forceinline__ const int* forced_row(const ActionArgs& a) {
+    return a.forced ? a.forced + (a.forced_td ? (a.horizon - a.k) * (long long)a.n : 0) : nullptr;
+}
+__device__ __forceinline__ int* chosen_row(const ActionArgs& a) {
+    return a.chosen ? a.chosen + (a.chosen_td ? (a.horizon - a.k) * (long long)a.n : 0) : nullptr;
+}
+
+// Block-wide residual fold and, for the finalizing launch, the stop test.
+// Every thread of the block must call this exactly once.
+template <class T>
+__device__ void iteration_epilogue(unsigned long long my, const ActionArgs& a, T eps, Ctl* ctl) {
+    using N = Num<T>;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(kFull, my, o);
+        my = other > my ? other : my;
+    }
+    __shared__ unsigned long long wmax[32];
+    __shared__ bool last;
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = my;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = wmax[i] > m ? wmax[i] : m;
+        if (m) atomicMax(&ctl->res_bits[a.k & 1], m);
+        last = false;
+        if (a.finalize) {
+            __threadfence();
+            last = atomicAdd(&ctl->arrive, 1u) == gridDim.x - 1;
+        }
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long rb = atomicAdd(&ctl->res_bits[a.k & 1], 0ull);
+        const T res = N::from_res_bits(rb);
+        ctl->k = a.k;
+        ctl->res_last = static_cast<double>(res);
+        ctl->res_bits[(a.k + 1) & 1] = 0ull;
+        if (a.work)
+            for (int i = 0; i < kWorkKinds; ++i) a.work[((a.k + 1) & 1) * kWorkKinds + i] = 0u;
+        ctl->arrive = 0u;
+        if (a.record_only) {
+            // the global residual is reduced across ranks by the sharded driver
+        } else if (a.finite) {
+            if (a.k >= a.horizon) ctl->done = 1;
+        } else if (res <= eps) {
+            ctl->done = 1;
+        } else if (a.k >= a.max_iterations) {
+            ctl->done = 1;
+            ctl->status = 1;
+        }
+        __threadfence();
+    }
+}
+
+// One thread per state of `states` (or of all local states when null), from
+// the per-column expectations q.
 template <class T>
 __global__ void __launch_bounds__(256)
-action_reduce(ActionArgs a, const T* __restrict__ q, const T* __restrict__ vin, T* __restrict__ vout,
-              const T* __restrict__ rewards, T discount, T eps, Ctl* __restrict__ ctl) {
+action_reduce(ActionArgs a, int nstates, const int* __restrict__ states, const T* __restrict__ q,
+              const T* __restrict__ vin, T* __restrict__ vout, const T* __restrict__ rewards, T discount, T eps,
+              Ctl* __restrict__ ctl) {
     using N = Num<T>;
     if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
-    const int* forced = a.forced ? a.forced + (a.forced_td ? (a.horizon - a.k) * (long long)a.n : 0) : nullptr;
-    int* chosen = a.chosen ? a.chosen + (a.chosen_td ? (a.horizon - a.k) * (long long)a.n : 0) : nullptr;
+    const int* forced = forced_row(a);
+    int* chosen = chosen_row(a);
     unsigned long long my = 0;
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.n; s += gridDim.x * blockDim.x) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nstates; i += gridDim.x * blockDim.x) {
+        const int s = states ? states[i] : i;
         const T prev = vin[a.state_begin + s];
         T best;
         int best_c = -1;
@@ -444,7 +511,7 @@ action_reduce(ActionArgs a, const T* __restrict__ q, const T* __restrict__ vin, 
             best_c = cb < ce ? cb : -1;
             for (int c = cb + 1; c < ce; ++c) {
                 const T x = q[c];
-                if (a.maximize ? (x > best) : (x < best)) {
+                if (a.maximize ? (x > best) : (x < best)) { // ties keep the lowest column
                     best = x;
                     best_c = c;
                 }
@@ -453,48 +520,208 @@ action_reduce(ActionArgs a, const T* __restrict__ q, const T* __restrict__ vin, 
         if (rewards) best = N::add(rewards[s], N::mul(discount, best));
         vout[a.state_begin + s] = best;
         if (chosen) chosen[s] = best_c;
-        const T res = fabs(N::sub(best, prev));
-        const unsigned long long rb = N::res_bits(res);
+        const unsigned long long rb = N::res_bits(fabs(N::sub(best, prev)));
         my = rb > my ? rb : my;
     }
-    // block max -> one atomic per block
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long other = __shfl_xor_sync(kFull, my, o);
-        my = other > my ? other : my;
-    }
-    __shared__ unsigned long long wmax[8];
-    __shared__ bool last;
-    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = my;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long m = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = wmax[i] > m ? wmax[i] : m;
-        if (m) atomicMax(&ctl->res_bits[a.k & 1], m);
-        __threadfence();
-        last = atomicAdd(&ctl->arrive, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence();
-        const unsigned long long rb = atomicAdd(&ctl->res_bits[a.k & 1], 0ull);
-        const T res = N::from_res_bits(rb);
-        ctl->k = a.k;
-        ctl->res_last = static_cast<double>(res);
-        ctl->res_bits[(a.k + 1) & 1] = 0ull;
-        if (a.work) a.work[(a.k + 1) & 1] = 0u;
-        ctl->arrive = 0u;
-        if (a.record_only) {
-            // global residual is reduced across ranks by the sharded driver
-        } else if (a.finite) {
-            if (a.k >= a.horizon) ctl->done = 1;
-        } else if (res <= eps) {
-            ctl->done = 1;
-        } else if (a.k >= a.max_iterations) {
-            ctl->done = 1;
-            ctl->status = 1;
+    iteration_epilogue<T>(my, a, eps, ctl);
+}
+
+// ---------------------------------------------------------------------------
+// Fused Bellman step for "short states": states whose columns all have <= 32
+// entries, packed by the host scheduler into state-aligned batches of <= 16
+// columns (slots padded with -1).  Per batch the warp runs the column O-max
+// of omax_short (same 3-deep pipeline), sums each column in row order, then
+// lane j reduces state j over its columns, applies frozen / forced /
+// reward, writes V_k and the chosen column and folds the residual — one
+// kernel per iteration, no q round trip.
+template <class T, bool kPess>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kShortBlocksPerSm)
+bellman_short(int nbatch, const int* __restrict__ slots, const int2* __restrict__ bstates,
+              const long long* __restrict__ colptr, const int* __restrict__ rows, const T* __restrict__ lower,
+              const T* __restrict__ gap, const T* __restrict__ rem, const T* __restrict__ vin, T* __restrict__ vout,
+              const T* __restrict__ rewards, T discount, T eps, ActionArgs a, Ctl* __restrict__ ctl) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    __shared__ T xs[kWarpsPerBlock][kShortBatch][kShortLen + 1];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
+    unsigned* work = a.work + (a.k & 1) * kWorkKinds + 1;
+    const int* forced = forced_row(a);
+    int* chosen = chosen_row(a);
+    const int* __restrict__ stateptr = a.stateptr;
+    unsigned long long myres = 0;
+
+    auto next_batch = [&]() -> int {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(work, 1u);
+        return nw + static_cast<int>(__shfl_sync(kFull, t, 0));
+    };
+    int bt = gw;
+    if (bt < nbatch) {
+        int nbt = next_batch();
+        // window: lane j < 16 -> slot j of batch bt, lane 16 + j -> slot j of batch nbt
+        int mc = -1, mlen = 0, ms0 = 0, mns = 0;
+        long long mbeg = 0;
+        T mrem = T(0);
+        auto load_meta = [&](int b) {
+            mc = -1;
+            mlen = 0;
+            mbeg = 0;
+            mrem = T(0);
+            ms0 = 0;
+            mns = 0;
+            if (b < nbatch) {
+                const int2 bi = __ldg(bstates + b);
+                ms0 = bi.x;
+                mns = bi.y;
+                mc = __ldg(slots + b * kShortBatch + (lane & (kShortBatch - 1)));
+                if (mc >= 0) {
+                    mbeg = __ldg(colptr + mc);
+                    mlen = static_cast<int>(__ldg(colptr + mc + 1) - mbeg);
+                    mrem = __ldg(rem + mc);
+                }
+            }
+        };
+        load_meta(lane < kShortBatch ? bt : nbt);
+        // state-side prefetch for the current batch (used at its end)
+        int s0 = 0, ns = 0, cs = 0, ce = 0, fz = 0, fc = -1;
+        T prev = T(0), rw = T(0);
+        auto load_states = [&]() {
+            s0 = __shfl_sync(kFull, ms0, 0);
+            ns = __shfl_sync(kFull, mns, 0);
+            if (lane < ns) {
+                const int s = s0 + lane;
+                cs = __ldg(stateptr + s);
+                ce = __ldg(stateptr + s + 1);
+                prev = __ldg(vin + a.state_begin + s);
+                fz = a.frozen ? a.frozen[s] : 0;
+                fc = forced ? __ldg(forced + s) : -1;
+                rw = rewards ? __ldg(rewards + s) : T(0);
+            }
+        };
+        load_states();
+
+        // pipeline prologue: data of slot 0, rows of slot 1
+        long long bn = __shfl_sync(kFull, mbeg, 0), bnn = __shfl_sync(kFull, mbeg, 1);
+        int Ln = __shfl_sync(kFull, mlen, 0), Lnn = __shfl_sync(kFull, mlen, 1);
+        int rowA = lane < Ln ? __ldg(rows + bn + lane) : 0;
+        T lc = T(0), gc = T(0), vc = T(0);
+        int Lc = Ln;
+        if (lane < Ln) {
+            lc = __ldg(lower + bn + lane);
+            gc = __ldg(gap + bn + lane);
+            vc = __ldg(vin + rowA);
         }
-        __threadfence();
+        bn = bnn;
+        Ln = Lnn;
+        rowA = lane < Ln ? __ldg(rows + bn + lane) : 0;
+        bnn = __shfl_sync(kFull, mbeg, 2);
+        Lnn = __shfl_sync(kFull, mlen, 2);
+
+        for (;;) {
+#pragma unroll 2
+            for (int s = 0; s < kShortBatch; ++s) {
+                T ln = T(0), gn = T(0), vn = T(0);
+                if (lane < Ln) {
+                    ln = __ldg(lower + bn + lane);
+                    gn = __ldg(gap + bn + lane);
+                    vn = __ldg(vin + rowA);
+                }
+                const int rowB = lane < Lnn ? __ldg(rows + bnn + lane) : 0;
+                const T r = __shfl_sync(kFull, mrem, s);
+                const bool valid = lane < Lc;
+                Bits key = valid ? order_key<T>(vc, kPess) : ~Bits(0);
+                T p = lc;
+                T avail = r, consumed = T(0);
+                for (int nsel = 0; avail > T(0) && nsel < Lc; ++nsel) {
+                    const int sel = warp_argmin_sentinel(key);
+                    const T gs = __shfl_sync(kFull, gc, sel);
+                    if (lane == sel) {
+                        p = N::add(lc, gc < avail ? gc : avail);
+                        key = ~Bits(0);
+                    }
+                    consumed = N::add(consumed, gs);
+                    avail = N::sub(r, consumed);
+                }
+                if (valid) xs[w][s][lane] = N::mul(vc, p);
+                lc = ln;
+                gc = gn;
+                vc = vn;
+                Lc = Ln;
+                rowA = rowB;
+                bn = bnn;
+                Ln = Lnn;
+                bnn = __shfl_sync(kFull, mbeg, s + 3);
+                Lnn = __shfl_sync(kFull, mlen, s + 3);
+            }
+            __syncwarp();
+            // column expectations in row order (omax.hpp:169-173): lane t -> slot t
+            T qv = T(0);
+            if (lane < kShortBatch && mc >= 0) {
+                for (int i = 0; i < mlen; ++i) qv = N::add(qv, xs[w][lane][i]);
+            }
+            __syncwarp();
+            // action reduction: lane j -> state s0 + j (bellman.hpp:88-115)
+            {
+                const int c0 = __shfl_sync(kFull, mc, 0);
+                const int lo = cs - c0, na = ce - cs;
+                const int maxa = __reduce_max_sync(kFull, lane < ns ? na : 0);
+                T best = __shfl_sync(kFull, qv, lane < ns ? lo : 0);
+                int bestc = lo;
+                for (int j = 1; j < maxa; ++j) {
+                    const T x = __shfl_sync(kFull, qv, lane < ns && j < na ? lo + j : 0);
+                    if (j < na && (a.maximize ? (x > best) : (x < best))) { // ties keep the lowest column
+                        best = x;
+                        bestc = lo + j;
+                    }
+                }
+                const T fq = __shfl_sync(kFull, qv, fc >= 0 && lane < ns ? fc - c0 : 0);
+                if (lane < ns) {
+                    const int s = s0 + lane;
+                    int bc;
+                    if (fz) {
+                        best = prev;
+                        bc = -1;
+                    } else if (fc >= 0) {
+                        best = fq;
+                        bc = fc;
+                    } else if (na <= 0) {
+                        best = prev;
+                        bc = -1;
+                    } else {
+                        bc = c0 + bestc;
+                    }
+                    if (rewards) best = N::add(rw, N::mul(discount, best));
+                    vout[a.state_begin + s] = best;
+                    if (chosen) chosen[s] = bc;
+                    const unsigned long long rb = N::res_bits(fabs(N::sub(best, prev)));
+                    myres = rb > myres ? rb : myres;
+                }
+            }
+            bt = nbt;
+            if (bt >= nbatch) break;
+            nbt = next_batch();
+            const int c2 = __shfl_down_sync(kFull, mc, kShortBatch);
+            const long long b2 = __shfl_down_sync(kFull, mbeg, kShortBatch);
+            const int l2 = __shfl_down_sync(kFull, mlen, kShortBatch);
+            const T r2 = __shfl_down_sync(kFull, mrem, kShortBatch);
+            const int s02 = __shfl_down_sync(kFull, ms0, kShortBatch);
+            const int ns2 = __shfl_down_sync(kFull, mns, kShortBatch);
+            if (lane < kShortBatch) {
+                mc = c2;
+                mbeg = b2;
+                mlen = l2;
+                mrem = r2;
+                ms0 = s02;
+                mns = ns2;
+            } else {
+                load_meta(nbt);
+            }
+            load_states();
+        }
     }
+    iteration_epilogue<T>(myres, a, eps, ctl);
 }
 
 template <class T>

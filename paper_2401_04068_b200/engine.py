@@ -96,7 +96,7 @@ _SIGNATURES = {
     "rimdp_solve_finish": ([_VP, _VP], C.c_int),
     "rimdp_solve_value_buffers": ([_VP, _VP, _VP], C.c_int),
     "rimdp_profile_enable": ([_VP, _I32], C.c_int),
-    "rimdp_profile_read": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
+    "rimdp_profile_read": ([_VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_bellman_step": ([_VP, _VP, _I32, _I32, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_column_values": ([_VP, _VP, _I32, _VP], C.c_int),
     "rimdp_random_imdp": ([_I32, _I32, _D, _D, C.c_uint64, _I32, _I32, _VP, _VP], C.c_int),
@@ -324,10 +324,11 @@ class DeviceModel:
         _check(load().rimdp_profile_enable(self._h, int(on)))
 
     def profile_read(self):
-        """(column-kernel ms, action-kernel ms, iterations, kernels per iteration) since the last read."""
-        c, a, it, kp = C.c_double(), C.c_double(), C.c_int64(), C.c_int32()
-        _check(load().rimdp_profile_read(self._h, C.byref(c), C.byref(a), C.byref(it), C.byref(kp)))
-        return c.value, a.value, it.value, kp.value
+        """Summed ms of (fused short-state kernel, per-column kernels, action kernel), iterations,
+        kernels per iteration — since the last read."""
+        f, c, a, it, kp = C.c_double(), C.c_double(), C.c_double(), C.c_int64(), C.c_int32()
+        _check(load().rimdp_profile_read(self._h, C.byref(f), C.byref(c), C.byref(a), C.byref(it), C.byref(kp)))
+        return f.value, c.value, a.value, it.value, kp.value
 
     def value_buffers(self):
         b0, b1 = C.c_void_p(), C.c_void_p()
