@@ -123,6 +123,7 @@ struct rimdp_model {
     std::vector<Infeasible> infeasible_cols;
     long long device_bytes = 0;
     int sm_count = 148;
+    int short_blocks_per_sm = 4;
     SolveState s;
 };
 
@@ -280,6 +281,7 @@ void init_common(rimdp_model* m, int device) {
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+    if (const char* e = getenv("RIMDP_SHORT_BLOCKS")) m->short_blocks_per_sm = atoi(e) == 5 ? 5 : 4;
 }
 
 // ---------------------------------------------------------------------------
@@ -397,8 +399,11 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     const T* rw = s.has_rewards ? s.rewards.as<T>() : nullptr;
     if (m->nbatch > 0) {
         a.finalize = m->nlong_states == 0;
-        const int blocks = grid_for((long long)m->nbatch, kWarpsPerBlock, m->sm_count, kShortBlocksPerSm);
-        auto kern = s.pess ? bellman_short<T, true> : bellman_short<T, false>;
+        // occupancy variant: 4 resident blocks (64 registers) or 5 (48 registers)
+        const int bps = m->short_blocks_per_sm;
+        const int blocks = grid_for((long long)m->nbatch, kWarpsPerBlock, m->sm_count, bps);
+        auto kern = bps == 5 ? (s.pess ? bellman_short<T, true, 5> : bellman_short<T, false, 5>)
+                             : (s.pess ? bellman_short<T, true, 4> : bellman_short<T, false, 4>);
         kern<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(
             m->nbatch, m->batch_slots.as<int>(), m->batch_states.as<int2>(), m->colptr.as<long long>(),
             m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), vin, vout, rw, (T)s.discount,

@@ -482,6 +482,49 @@ __device__ void iteration_epilogue(unsigned long long my, const ActionArgs& a, T
     }
 }
 
+// Barrier-free variant for kernels whose warps finish at different times:
+// warps fold into shared memory and the last warp of the block to arrive
+// carries the block's result to ctl (and, when finalizing, the stop test).
+// `s_res` / `s_arrived` must be zeroed before the block's first __syncthreads.
+template <class T>
+__device__ void warp_epilogue(unsigned long long my, const ActionArgs& a, T eps, Ctl* ctl,
+                              unsigned long long* s_res, unsigned* s_arrived) {
+    using N = Num<T>;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(kFull, my, o);
+        my = other > my ? other : my;
+    }
+    if ((threadIdx.x & 31) != 0) return;
+    if (my) atomicMax(s_res, my);
+    __threadfence_block();
+    if (atomicAdd(s_arrived, 1u) != (blockDim.x >> 5) - 1) return;
+    __threadfence_block();
+    const unsigned long long m = *reinterpret_cast<volatile unsigned long long*>(s_res);
+    if (m) atomicMax(&ctl->res_bits[a.k & 1], m);
+    if (!a.finalize) return;
+    __threadfence();
+    if (atomicAdd(&ctl->arrive, 1u) != gridDim.x - 1) return;
+    __threadfence();
+    const unsigned long long rb = atomicAdd(&ctl->res_bits[a.k & 1], 0ull);
+    const T res = N::from_res_bits(rb);
+    ctl->k = a.k;
+    ctl->res_last = static_cast<double>(res);
+    ctl->res_bits[(a.k + 1) & 1] = 0ull;
+    if (a.work)
+        for (int i = 0; i < kWorkKinds; ++i) a.work[((a.k + 1) & 1) * kWorkKinds + i] = 0u;
+    ctl->arrive = 0u;
+    if (a.record_only) {
+    } else if (a.finite) {
+        if (a.k >= a.horizon) ctl->done = 1;
+    } else if (res <= eps) {
+        ctl->done = 1;
+    } else if (a.k >= a.max_iterations) {
+        ctl->done = 1;
+        ctl->status = 1;
+    }
+    __threadfence();
+}
+
 // One thread per state of `states` (or of all local states when null), from
 // the per-column expectations q.
 template <class T>
@@ -534,8 +577,8 @@ action_reduce(ActionArgs a, int nstates, const int* __restrict__ states, const T
 // lane j reduces state j over its columns, applies frozen / forced /
 // reward, writes V_k and the chosen column and folds the residual — one
 // kernel per iteration, no q round trip.
-template <class T, bool kPess>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, kShortBlocksPerSm)
+template <class T, bool kPess, int kBlocks>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kBlocks)
 bellman_short(int nbatch, const int* __restrict__ slots, const int2* __restrict__ bstates,
               const long long* __restrict__ colptr, const int* __restrict__ rows, const T* __restrict__ lower,
               const T* __restrict__ gap, const T* __restrict__ rem, const T* __restrict__ vin, T* __restrict__ vout,
@@ -544,6 +587,13 @@ bellman_short(int nbatch, const int* __restrict__ slots, const int2* __restrict_
     using Bits = typename N::Bits;
     if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
     __shared__ T xs[kWarpsPerBlock][kShortBatch][kShortLen + 1];
+    __shared__ unsigned long long s_res;
+    __shared__ unsigned s_arrived;
+    if (threadIdx.x == 0) {
+        s_res = 0ull;
+        s_arrived = 0u;
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
     unsigned* work = a.work + (a.k & 1) * kWorkKinds + 1;
@@ -721,7 +771,7 @@ bellman_short(int nbatch, const int* __restrict__ slots, const int2* __restrict_
             load_states();
         }
     }
-    iteration_epilogue<T>(myres, a, eps, ctl);
+    warp_epilogue<T>(myres, a, eps, ctl, &s_res, &s_arrived);
 }
 
 template <class T>
