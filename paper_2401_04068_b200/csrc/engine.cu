@@ -184,7 +184,12 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         (len <= kShortLen ? cs : cl).push_back(c);
     }
     const std::vector<int>& sp = m->h_stateptr;
+    // The fused state-aligned kernel is opt-in (RIMDP_FUSED=1): measured on
+    // B200 (profiles/round1) the split omax_short + action_reduce pair is faster.
+    const char* fz = getenv("RIMDP_FUSED");
+    const bool fused = fz && atoi(fz) != 0;
     auto short_state = [&](int s) {
+        if (!fused) return false;
         const int na = sp[s + 1] - sp[s];
         if (na < 1 || na > kShortBatch) return false;
         for (int c = sp[s]; c < sp[s + 1]; ++c)
