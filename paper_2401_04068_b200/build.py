@@ -81,5 +81,32 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "dropin_parity.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "_build", "dropin_parity")
+REFERENCE_INCLUDE = os.path.join(os.environ.get("RIMDP_REFERENCE", "/root/reference"), "proj", "include")
+
+
+def build_cpp_tests(force: bool = False) -> str | None:
+    """Compile the C++ drop-in parity program (tests/cpp/dropin_parity.cpp):
+    include/rimdp_b200/dropin.hpp over the engine library, checked against the
+    reference's own headers compiled in as the oracle.  Needs the reference
+    headers (present in the build container, absent on the GPU box, where the
+    prebuilt binary travels with the snapshot); returns None without them."""
+    if not os.path.isdir(REFERENCE_INCLUDE):
+        return None
+    deps_ = [CPP_TEST_SRC, os.path.join(INCLUDE, "rimdp_b200", "dropin.hpp"), os.path.join(INCLUDE, "rimdp_b200.h")]
+    if (not force and os.path.exists(CPP_TEST_BIN) and
+            all(os.path.getmtime(d) <= os.path.getmtime(CPP_TEST_BIN) for d in deps_)):
+        return CPP_TEST_BIN
+    os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
+    stubs = os.path.join(ROOT, "oracle", "stubs")  # Boost stub: Rational is never instantiated
+    cmd = ["g++", "-std=gnu++20", "-O2", "-Wall", "-Wextra", "-Wno-unused-parameter", "-ffp-contract=off",
+           "-I", stubs, "-I", REFERENCE_INCLUDE, "-I", INCLUDE, CPP_TEST_SRC, "-o", CPP_TEST_BIN,
+           "-L", LIBDIR, "-lrimdp_b200", f"-Wl,-rpath,{LIBDIR}", "-Wl,-rpath,$ORIGIN/../../../paper_2401_04068_b200/lib",
+           "-pthread"]
+    subprocess.run(cmd, check=True)
+    return CPP_TEST_BIN
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose=True))

@@ -623,6 +623,8 @@ int step_t(rimdp_model* m, const void* v_in, int pess, int maxi, const uint8_t* 
 
 template <class T>
 int column_values_t(rimdp_model* m, const void* v_in, int pess, void* q_out) {
+    // every column is evaluated: the first infeasible one throws (omax.hpp:72-80)
+    if (!m->infeasible_cols.empty()) return report_infeasible(&m->infeasible_cols[0], m->dtype);
     SolveState& s = m->s;
     s.v[0].ensure(sizeof(T) * m->n_global);
     s.q.ensure(sizeof(T) * std::max(1, m->ncols));
