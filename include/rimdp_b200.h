@@ -107,10 +107,18 @@ typedef struct rimdp_gen_config {
 } rimdp_gen_config;
 
 int rimdp_model_generate(const rimdp_gen_config* cfg, rimdp_model** out);
-/* Host copies of a generated model's columns [col_begin, col_end) for sampled
- * parity checks (colptr relative to col_begin's first entry). */
+/* The same generator on the host (bit-identical columns), for sampled and
+ * scaled-down parity checks against the CPU reference.  Two-phase: with
+ * null arrays only the sizes are returned.  stateptr has (state_end -
+ * state_begin) + 1 entries, colptr num_cols + 1. */
+int rimdp_generate_host(const rimdp_gen_config* cfg, int32_t* num_cols, int64_t* nnz, int32_t* stateptr,
+                        int64_t* colptr, int32_t* rowval, void* lower, void* upper);
+/* Host copies of columns [col_begin, col_end) of a device store, as stored:
+ * rows, lower bounds and gaps (upper - lower, rounded in dtype; the store
+ * keeps gaps).  colptr_out (col_end - col_begin
+ * + 1 entries) is relative to col_begin's first entry. */
 int rimdp_model_read_columns(rimdp_model* model, int32_t col_begin, int32_t col_end, int64_t* colptr_out,
-                             int32_t* rowval_out, void* lower_out, void* upper_out);
+                             int32_t* rowval_out, void* lower_out, void* gap_out);
 
 typedef struct rimdp_model_info {
     rimdp_dtype dtype;

@@ -9,11 +9,14 @@
 //   parallel_for_index (per-step thread fork)    parallel.hpp:27-68  -> CUDA grid
 #include "rimdp_b200.h"
 
+#include "generator.cuh"
 #include "omax_kernels.cuh"
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -75,6 +78,23 @@ struct DevBuf {
     U* as() const { return static_cast<U*>(p); }
 };
 
+// Column classes of the scheduler: <= 32 entries ->
+// warp kernel (omax_short); longer columns whose greedy stops after a few
+// picks -> exact warp kernel (omax_long); the rest -> one CTA per column,
+// sorted (omax_sorted), by power-of-two size class 2^6 .. 2^13.
+constexpr int kSortedMinLog = 6, kSortedMaxLog = 13, kSortedClasses = kSortedMaxLog - kSortedMinLog + 1;
+constexpr double kExactPickBudget = 4.0;
+
+struct ColumnLists {
+    DevBuf short_list, exact_list, sorted_list[kSortedClasses];
+    int n_short = 0, n_exact = 0, n_sorted[kSortedClasses] = {};
+    int total_sorted() const {
+        int t = 0;
+        for (int i = 0; i < kSortedClasses; ++i) t += n_sorted[i];
+        return t;
+    }
+};
+
 struct Infeasible {
     int col;
     int kind;
@@ -114,10 +134,10 @@ struct rimdp_model {
     int ncols = 0;
     long long nnz = 0;
     int maxlen = 0;
-    DevBuf stateptr, colptr, rows, lower, gap, rem, infeasible, quoted, short_list, long_list, scratch;
-    DevBuf q_short_list, q_long_list, batch_slots, batch_states, long_states;
-    int nshort = 0, nlong = 0;                // all columns by length (column_values)
-    int nq_short = 0, nq_long = 0;            // columns of long states (q path)
+    DevBuf stateptr, colptr, rows, lower, gap, rem, maxgap, infeasible, quoted, scratch;
+    DevBuf batch_slots, batch_states, long_states;
+    ColumnLists all;                          // every column by class (rimdp_column_values)
+    ColumnLists qp;                           // columns of the q-path states (iterations)
     int nbatch = 0, nlong_states = 0;         // fused short-state batches / q-path states
     std::vector<int> h_stateptr;
     std::vector<Infeasible> infeasible_cols;
@@ -165,27 +185,78 @@ void upload_list(rimdp_model* m, DevBuf& buf, const std::vector<U>& v) {
     if (!v.empty()) CK(cudaMemcpyAsync(buf.p, v.data(), sizeof(U) * v.size(), cudaMemcpyHostToDevice, m->stream));
 }
 
+// Routing mode for long columns: RIMDP_LONG=exact|sorted forces one path (tests).
+int long_mode() {
+    const char* e = getenv("RIMDP_LONG");
+    if (!e) return 0;
+    if (!strcmp(e, "exact")) return 1;
+    if (!strcmp(e, "sorted")) return 2;
+    return 0;
+}
+
+// Class of one column given its length, remainder and largest gap.
+//   0: short   1: exact long   2 + i: sorted, size class 2^(kSortedMinLog + i)
+int column_class(long long len, double rem, double maxgap, int mode) {
+    if (len <= kShortLen) return 0;
+    if (len > (1ll << kSortedMaxLog)) return 1; // beyond the largest CTA sort: exact warp kernel
+    bool sorted;
+    if (mode) {
+        sorted = mode == 2;
+    } else {
+        // the greedy needs at least rem / maxgap picks; few picks -> exact argmin kernel
+        sorted = rem > 0 && (maxgap <= 0 || rem > kExactPickBudget * maxgap);
+    }
+    if (!sorted) return 1;
+    int lg = kSortedMinLog;
+    while ((1ll << lg) < len) ++lg;
+    return 2 + (lg - kSortedMinLog);
+}
+
+void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, const std::vector<signed char>& cls) {
+    std::vector<int> sh, ex, so[kSortedClasses];
+    for (int c : cols) {
+        const int k = cls[c];
+        if (k == 0) sh.push_back(c);
+        else if (k == 1) ex.push_back(c);
+        else so[k - 2].push_back(c);
+    }
+    L.n_short = (int)sh.size();
+    L.n_exact = (int)ex.size();
+    upload_list(m, L.short_list, sh);
+    upload_list(m, L.exact_list, ex);
+    for (int i = 0; i < kSortedClasses; ++i) {
+        L.n_sorted[i] = (int)so[i].size();
+        upload_list(m, L.sorted_list[i], so[i]);
+    }
+}
+
 // Column scheduler:
-//  * every column is routed by length: <= 32 entries -> warp-per-column
-//    lane-per-entry kernel, longer -> warp-per-column strided kernel
-//    (these lists serve rimdp_column_values);
-//  * for iterations, runs of consecutive "short states" (<= 16 columns, all
-//    columns <= 32 entries) are packed into state-aligned batches of <= 16
-//    column slots for the fused bellman_short kernel; the remaining "long
-//    states" take the q path (column kernels + action_reduce).
+//  * every column is classified by length and by how many greedy picks it
+//    can need (column_class); the lists of all columns serve
+//    rimdp_column_values;
+//  * for iterations, with RIMDP_FUSED=1, runs of consecutive "short states"
+//    (<= 16 columns, all columns <= 32 entries) are packed into state-aligned
+//    batches of <= 16 column slots for the fused bellman_short kernel; the
+//    remaining states take the q path (column kernels + action_reduce).
+template <class T>
 void build_schedule(rimdp_model* m, const long long* h_colptr) {
-    std::vector<int> cs, cl, qs, ql, slots, lstates;
-    std::vector<int2> bstates;
-    cs.reserve(m->ncols);
+    std::vector<T> h_rem(m->ncols), h_maxgap(m->ncols);
+    if (m->ncols > 0) {
+        CK(cudaMemcpyAsync(h_rem.data(), m->rem.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaMemcpyAsync(h_maxgap.data(), m->maxgap.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+    }
+    const int mode = long_mode();
+    std::vector<signed char> cls(m->ncols);
+    std::vector<int> allc(m->ncols), qc;
     int maxlen = 0;
     for (int c = 0; c < m->ncols; ++c) {
         const long long len = h_colptr[c + 1] - h_colptr[c];
         maxlen = (int)std::max<long long>(maxlen, len);
-        (len <= kShortLen ? cs : cl).push_back(c);
+        cls[c] = (signed char)column_class(len, (double)h_rem[c], (double)h_maxgap[c], mode);
+        allc[c] = c;
     }
     const std::vector<int>& sp = m->h_stateptr;
-    // The fused state-aligned kernel is opt-in (RIMDP_FUSED=1): measured on
-    // B200 (profiles/round1) the split omax_short + action_reduce pair is faster.
     const char* fz = getenv("RIMDP_FUSED");
     const bool fused = fz && atoi(fz) != 0;
     auto short_state = [&](int s) {
@@ -193,9 +264,11 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         const int na = sp[s + 1] - sp[s];
         if (na < 1 || na > kShortBatch) return false;
         for (int c = sp[s]; c < sp[s + 1]; ++c)
-            if (h_colptr[c + 1] - h_colptr[c] > kShortLen) return false;
+            if (cls[c] != 0) return false;
         return true;
     };
+    std::vector<int> slots, lstates;
+    std::vector<int2> bstates;
     int s0 = -1, used = 0;
     auto close_batch = [&]() {
         if (s0 < 0) return;
@@ -207,7 +280,7 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         if (!short_state(s)) {
             close_batch();
             lstates.push_back(s);
-            for (int c = sp[s]; c < sp[s + 1]; ++c) (h_colptr[c + 1] - h_colptr[c] <= kShortLen ? qs : ql).push_back(c);
+            for (int c = sp[s]; c < sp[s + 1]; ++c) qc.push_back(c);
             continue;
         }
         const int na = sp[s + 1] - sp[s];
@@ -222,16 +295,10 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     }
     close_batch();
     m->maxlen = maxlen;
-    m->nshort = (int)cs.size();
-    m->nlong = (int)cl.size();
-    m->nq_short = (int)qs.size();
-    m->nq_long = (int)ql.size();
+    fill_lists(m, m->all, allc, cls);
+    fill_lists(m, m->qp, qc, cls);
     m->nbatch = (int)bstates.size();
     m->nlong_states = (int)lstates.size();
-    upload_list(m, m->short_list, cs);
-    upload_list(m, m->long_list, cl);
-    upload_list(m, m->q_short_list, qs);
-    upload_list(m, m->q_long_list, ql);
     upload_list(m, m->batch_slots, slots);
     upload_list(m, m->batch_states, bstates);
     upload_list(m, m->long_states, lstates);
@@ -243,6 +310,7 @@ void prepare(rimdp_model* m) {
     m->rem.ensure(sizeof(T) * std::max(1, m->ncols));
     m->infeasible.ensure(std::max(1, m->ncols));
     m->quoted.ensure(sizeof(T) * std::max(1, m->ncols));
+    m->maxgap.ensure(sizeof(T) * std::max(1, m->ncols));
     m->scratch.ensure(64);
     CK(cudaMemsetAsync(m->scratch.p, 0, 64, m->stream));
     int* counters = m->scratch.as<int>();
@@ -252,7 +320,7 @@ void prepare(rimdp_model* m) {
     if (m->ncols > 0)
         prepare_columns<T><<<grid_for(m->ncols, 128, m->sm_count, 16), 128, 0, m->stream>>>(
             m->ncols, m->colptr.as<long long>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(),
-            m->infeasible.as<unsigned char>(), m->quoted.as<T>(), counters);
+            m->infeasible.as<unsigned char>(), m->quoted.as<T>(), m->maxgap.as<T>(), counters);
     CK(cudaGetLastError());
     int h[2] = {0, 0};
     CK(cudaMemcpyAsync(h, counters, sizeof h, cudaMemcpyDeviceToHost, m->stream));
@@ -345,23 +413,55 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     s.active = true;
 }
 
-// Per-column expectations q for the columns in the two length-routed lists.
+template <class T, bool P, int LG>
+void launch_sorted_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
+    using Sh = SortedShape<LG>;
+    auto k = omax_sorted<T, P, LG>;
+    const size_t smem = Sh::template smem<T>();
+    static bool configured[64] = {};
+    static int per_sm[64] = {};
+    const int dev = m->device & 63;
+    if (!configured[dev]) {
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, Sh::threads, smem));
+        per_sm[dev] = std::max(per_sm[dev], 1);
+        configured[dev] = true;
+    }
+    const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
+    k<<<blocks, Sh::threads, smem, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+                                                m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
+}
+
+template <class T, bool P, int LG = kSortedMinLog>
+void launch_sorted(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl) {
+    if constexpr (LG <= kSortedMaxLog) {
+        const int i = LG - kSortedMinLog;
+        if (L.n_sorted[i] > 0) launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+        launch_sorted<T, P, LG + 1>(m, L, V, q, ctl);
+    }
+}
+
+// Per-column expectations q for the columns of one set of class lists.
 template <class T>
-void launch_columns(rimdp_model* m, int ns, const DevBuf& sl, int nl, const DevBuf& ll, const T* V, T* q, Ctl* ctl,
-                    bool pess, unsigned* work) {
-    if (ns > 0) {
-        const int blocks = grid_for(ns, kShortBatch * kWarpsPerBlock, m->sm_count, 5);
+void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
+    if (L.n_short > 0) {
+        const int blocks = grid_for(L.n_short, kShortBatch * kWarpsPerBlock, m->sm_count, 5);
         auto k = pess ? omax_short<T, true> : omax_short<T, false>;
-        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(ns, sl.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
-                                                          m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl,
-                                                          work);
+        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(L.n_short, L.short_list.as<int>(), m->colptr.as<long long>(),
+                                                          m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
+                                                          m->rem.as<T>(), V, q, ctl, work);
     }
-    if (nl > 0) {
-        const int blocks = grid_for(nl, kWarpsPerBlock, m->sm_count, 8);
+    if (L.n_exact > 0) {
+        const int blocks = grid_for(L.n_exact, kWarpsPerBlock, m->sm_count, 8);
         auto k = pess ? omax_long<T, true> : omax_long<T, false>;
-        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(nl, ll.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
-                                                         m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
+        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(L.n_exact, L.exact_list.as<int>(), m->colptr.as<long long>(),
+                                                         m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
+                                                         m->rem.as<T>(), V, q, ctl);
     }
+    if (pess)
+        launch_sorted<T, true>(m, L, V, q, ctl);
+    else
+        launch_sorted<T, false>(m, L, V, q, ctl);
 }
 
 // One Bellman iteration: [q path for long states: column kernels] ->
@@ -415,8 +515,7 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
             (T)s.eps, a, ctl);
     }
     if (ev) CK(cudaEventRecord(ev[1], m->stream));
-    launch_columns<T>(m, m->nq_short, m->q_short_list, m->nq_long, m->q_long_list, vin, s.q.as<T>(), ctl, s.pess,
-                      work);
+    launch_columns<T>(m, m->qp, vin, s.q.as<T>(), ctl, s.pess, work);
     if (ev) CK(cudaEventRecord(ev[2], m->stream));
     if (m->nlong_states > 0) {
         a.finalize = 1;
@@ -428,7 +527,9 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
 }
 
 int kernels_per_iteration(const rimdp_model* m) {
-    return (m->nbatch > 0) + (m->nq_short > 0) + (m->nq_long > 0) + (m->nlong_states > 0);
+    int k = (m->nbatch > 0) + (m->qp.n_short > 0) + (m->qp.n_exact > 0) + (m->nlong_states > 0);
+    for (int i = 0; i < kSortedClasses; ++i) k += m->qp.n_sorted[i] > 0;
+    return k;
 }
 
 // First infeasible column that a step would evaluate (bellman.hpp:88-112:
@@ -631,8 +732,7 @@ int column_values_t(rimdp_model* m, const void* v_in, int pess, void* q_out) {
     CK(cudaMemcpyAsync(s.v[0].p, v_in, sizeof(T) * m->n_global, cudaMemcpyHostToDevice, m->stream));
     s.work.ensure(2 * kWorkKinds * sizeof(unsigned));
     CK(cudaMemsetAsync(s.work.p, 0, 2 * kWorkKinds * sizeof(unsigned), m->stream));
-    launch_columns<T>(m, m->nshort, m->short_list, m->nlong, m->long_list, s.v[0].as<T>(), s.q.as<T>(), nullptr,
-                      pess != 0, s.work.as<unsigned>());
+    launch_columns<T>(m, m->all, s.v[0].as<T>(), s.q.as<T>(), nullptr, pess != 0, s.work.as<unsigned>());
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(q_out, s.q.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
@@ -707,11 +807,11 @@ int rimdp_model_create(const rimdp_model_desc* d, rimdp_model** out) {
             CK(cudaMemcpyAsync(m->lower.p, d->lower, es * d->nnz, cudaMemcpyHostToDevice, m->stream));
             CK(cudaMemcpyAsync(m->gap.p, d->upper, es * d->nnz, cudaMemcpyHostToDevice, m->stream));
         }
-        build_schedule(m.get(), reinterpret_cast<const long long*>(d->colptr));
         DISPATCH(m, prepare, m.get());
+        DISPATCH(m, build_schedule, m.get(), reinterpret_cast<const long long*>(d->colptr));
         m->device_bytes = (long long)(m->stateptr.bytes + m->colptr.bytes + m->rows.bytes + m->lower.bytes +
                                       m->gap.bytes + m->rem.bytes + m->infeasible.bytes + m->quoted.bytes +
-                                      m->short_list.bytes + m->long_list.bytes);
+                                      m->maxgap.bytes);
         *out = m.release();
         return RIMDP_OK;
     });
@@ -744,9 +844,9 @@ int rimdp_model_info_get(rimdp_model* m, rimdp_model_info* o) {
     o->max_column_length = m->maxlen;
     o->num_infeasible_columns = (int)m->infeasible_cols.size();
     o->device_bytes = m->device_bytes;
-    o->short_columns = m->nshort;
-    o->mid_columns = 0;
-    o->long_columns = m->nlong;
+    o->short_columns = m->all.n_short;
+    o->mid_columns = m->all.n_exact;
+    o->long_columns = m->all.total_sorted();
     return RIMDP_OK;
 }
 
@@ -896,16 +996,203 @@ int rimdp_column_values(rimdp_model* m, const void* v_in, int32_t pess, void* q_
     });
 }
 
+} // extern "C"
+
+// ---------------------------------------------------------------------------
+// Synthetic stores generated in HBM (generator.cuh)
+
+namespace {
+
+__global__ void gen_lengths(rimdp_gen::Params p, long long col0, int ncols, const unsigned long long* cdf,
+                            int* len) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x)
+        len[c] = rimdp_gen::column_length(p, reinterpret_cast<const uint64_t*>(cdf), col0 + c);
+}
+
+template <class T>
+__global__ void gen_columns(rimdp_gen::Params p, long long col0, int ncols, const long long* colptr, int* rows,
+                            T* lower, T* upper) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+        const long long b = colptr[c];
+        const int k = static_cast<int>(colptr[c + 1] - b);
+        rimdp_gen::write_column<T>(p, col0 + c, k, rows + b, lower + b, upper + b);
+    }
+}
+
+struct GenSetup {
+    rimdp_gen::Params p{};
+    int sb = 0, se = 0, ncols = 0;
+    long long col0 = 0;
+    std::vector<unsigned long long> cdf;
+};
+
+int gen_setup(const rimdp_gen_config* cfg, GenSetup& g) {
+    if (!cfg) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null config");
+    if (cfg->dtype != RIMDP_F64 && cfg->dtype != RIMDP_F32) return fail(RIMDP_ERR_INVALID_ARGUMENT, "unknown dtype");
+    if (cfg->num_states <= 0 || cfg->actions <= 0) return fail(RIMDP_ERR_INVALID_ARGUMENT, "bad model size");
+    if ((long long)cfg->num_states * cfg->actions > INT32_MAX)
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "more than 2^31-1 columns");
+    g.sb = cfg->state_begin;
+    g.se = cfg->state_end;
+    if (g.sb == 0 && g.se == 0) g.se = cfg->num_states;
+    if (g.sb < 0 || g.se > cfg->num_states || g.sb > g.se)
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "bad shard [%d, %d)", g.sb, g.se);
+    g.p.num_states = cfg->num_states;
+    g.p.actions = cfg->actions;
+    g.p.law = cfg->law;
+    g.p.support = cfg->support;
+    g.p.kmax = cfg->kmax;
+    g.p.lower_scale = cfg->lower_scale;
+    g.p.upper_scale = cfg->upper_scale;
+    g.p.seed = cfg->seed;
+    if (cfg->law == 0) {
+        if (cfg->support <= 0) return fail(RIMDP_ERR_INVALID_ARGUMENT, "law 0 needs support > 0");
+    } else if (cfg->law == 1) {
+        if (cfg->kmax <= 0 || cfg->kmax > rimdp_gen::kMaxK)
+            return fail(RIMDP_ERR_INVALID_ARGUMENT, "kmax must be in [1, %d]", rimdp_gen::kMaxK);
+        // cdf[k-1] = floor(2^64 P(K <= k)), P(K = k) ~ k^-alpha
+        std::vector<long double> w(cfg->kmax);
+        long double z = 0;
+        for (int k = 1; k <= cfg->kmax; ++k) z += (w[k - 1] = powl((long double)k, -(long double)cfg->alpha));
+        g.cdf.resize(cfg->kmax);
+        long double acc = 0;
+        for (int k = 1; k <= cfg->kmax; ++k) {
+            acc += w[k - 1];
+            const long double f = acc / z * 18446744073709551616.0L;
+            g.cdf[k - 1] = (k == cfg->kmax || f >= 18446744073709551615.0L) ? ~0ull : (unsigned long long)f;
+        }
+    } else {
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "unknown law %d", cfg->law);
+    }
+    g.ncols = (g.se - g.sb) * cfg->actions;
+    g.col0 = (long long)g.sb * cfg->actions;
+    return RIMDP_OK;
+}
+
+template <class T>
+void generate_t(rimdp_model* m, const GenSetup& g) {
+    const int nc = g.ncols;
+    DevBuf d_cdf, d_len;
+    std::vector<long long> h_colptr(nc + 1, 0);
+    if (g.p.law == 1) {
+        d_cdf.ensure(sizeof(unsigned long long) * g.cdf.size());
+        CK(cudaMemcpyAsync(d_cdf.p, g.cdf.data(), sizeof(unsigned long long) * g.cdf.size(), cudaMemcpyHostToDevice,
+                           m->stream));
+        d_len.ensure(sizeof(int) * std::max(1, nc));
+        if (nc > 0)
+            gen_lengths<<<grid_for(nc, 256, m->sm_count, 8), 256, 0, m->stream>>>(g.p, g.col0, nc,
+                                                                                d_cdf.as<unsigned long long>(),
+                                                                                d_len.as<int>());
+        CK(cudaGetLastError());
+        std::vector<int> len(nc);
+        if (nc > 0) CK(cudaMemcpyAsync(len.data(), d_len.p, sizeof(int) * nc, cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        for (int c = 0; c < nc; ++c) h_colptr[c + 1] = h_colptr[c] + len[c];
+    } else {
+        const int k = std::min(g.p.support, g.p.num_states);
+        for (int c = 0; c < nc; ++c) h_colptr[c + 1] = h_colptr[c] + k;
+    }
+    const long long nnz = h_colptr[nc];
+    m->nnz = nnz;
+    m->ncols = nc;
+    m->n = g.se - g.sb;
+    m->n_global = g.p.num_states;
+    m->state_begin = g.sb;
+    m->h_stateptr.resize(m->n + 1);
+    for (int s = 0; s <= m->n; ++s) m->h_stateptr[s] = s * g.p.actions;
+    m->stateptr.ensure(sizeof(int) * (m->n + 1));
+    m->colptr.ensure(sizeof(long long) * (nc + 1));
+    m->rows.ensure(sizeof(int) * std::max<long long>(1, nnz));
+    m->lower.ensure(sizeof(T) * std::max<long long>(1, nnz));
+    m->gap.ensure(sizeof(T) * std::max<long long>(1, nnz));
+    CK(cudaMemcpyAsync(m->stateptr.p, m->h_stateptr.data(), sizeof(int) * (m->n + 1), cudaMemcpyHostToDevice,
+                       m->stream));
+    CK(cudaMemcpyAsync(m->colptr.p, h_colptr.data(), sizeof(long long) * (nc + 1), cudaMemcpyHostToDevice,
+                       m->stream));
+    if (nc > 0)
+        gen_columns<T><<<grid_for(nc, 128, m->sm_count, 16), 128, 0, m->stream>>>(
+            g.p, g.col0, nc, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>());
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(m->stream));
+    prepare<T>(m);
+    build_schedule<T>(m, h_colptr.data());
+    m->device_bytes = (long long)(m->stateptr.bytes + m->colptr.bytes + m->rows.bytes + m->lower.bytes +
+                                  m->gap.bytes + m->rem.bytes + m->infeasible.bytes + m->quoted.bytes +
+                                  m->maxgap.bytes);
+}
+
+template <class T>
+int generate_host_t(const GenSetup& g, int32_t* num_cols, int64_t* nnz_out, int32_t* stateptr, int64_t* colptr,
+                    int32_t* rowval, void* lower, void* upper) {
+    const int nc = g.ncols;
+    std::vector<long long> cp(nc + 1, 0);
+    for (int c = 0; c < nc; ++c)
+        cp[c + 1] = cp[c] + rimdp_gen::column_length(g.p, reinterpret_cast<const uint64_t*>(g.cdf.data()), g.col0 + c);
+    if (num_cols) *num_cols = nc;
+    if (nnz_out) *nnz_out = cp[nc];
+    if (!colptr) return RIMDP_OK;
+    for (int c = 0; c <= nc; ++c) colptr[c] = cp[c];
+    if (stateptr)
+        for (int s = 0; s <= g.se - g.sb; ++s) stateptr[s] = s * g.p.actions;
+    if (rowval && lower && upper)
+        for (int c = 0; c < nc; ++c)
+            rimdp_gen::write_column<T>(g.p, g.col0 + c, (int)(cp[c + 1] - cp[c]), rowval + cp[c],
+                                       static_cast<T*>(lower) + cp[c], static_cast<T*>(upper) + cp[c]);
+    return RIMDP_OK;
+}
+
+} // namespace
+
+extern "C" {
+
 int rimdp_model_generate(const rimdp_gen_config* cfg, rimdp_model** out) {
-    (void)cfg;
-    (void)out;
-    return fail(RIMDP_ERR_INTERNAL, "rimdp_model_generate: not built in this configuration");
+    return guarded([&]() -> int {
+        if (!out) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+        GenSetup g;
+        if (int st = gen_setup(cfg, g)) return st;
+        std::unique_ptr<rimdp_model> m(new rimdp_model);
+        m->dtype = cfg->dtype;
+        init_common(m.get(), cfg->device);
+        DeviceGuard dg(m->device);
+        if (m->dtype == RIMDP_F64)
+            generate_t<double>(m.get(), g);
+        else
+            generate_t<float>(m.get(), g);
+        *out = m.release();
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_generate_host(const rimdp_gen_config* cfg, int32_t* num_cols, int64_t* nnz, int32_t* stateptr,
+                        int64_t* colptr, int32_t* rowval, void* lower, void* upper) {
+    return guarded([&]() -> int {
+        GenSetup g;
+        if (int st = gen_setup(cfg, g)) return st;
+        return cfg->dtype == RIMDP_F64 ? generate_host_t<double>(g, num_cols, nnz, stateptr, colptr, rowval, lower, upper)
+                                       : generate_host_t<float>(g, num_cols, nnz, stateptr, colptr, rowval, lower, upper);
+    });
 }
 
 int rimdp_model_read_columns(rimdp_model* m, int32_t cb, int32_t ce, int64_t* colptr_out, int32_t* rowval_out,
-                             void* lower_out, void* upper_out) {
-    (void)m; (void)cb; (void)ce; (void)colptr_out; (void)rowval_out; (void)lower_out; (void)upper_out;
-    return fail(RIMDP_ERR_INTERNAL, "rimdp_model_read_columns: not built in this configuration");
+                             void* lower_out, void* gap_out) {
+    if (!m || !colptr_out) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    if (cb < 0 || ce > m->ncols || cb > ce) return fail(RIMDP_ERR_INVALID_ARGUMENT, "bad column range");
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        std::vector<long long> cp(ce - cb + 1);
+        CK(cudaMemcpy(cp.data(), m->colptr.as<long long>() + cb, sizeof(long long) * cp.size(), cudaMemcpyDeviceToHost));
+        const long long b = cp[0], cnt = cp.back() - cp[0];
+        for (size_t i = 0; i < cp.size(); ++i) colptr_out[i] = cp[i] - b;
+        const size_t es = elem_size(m->dtype);
+        if (cnt > 0) {
+            if (rowval_out)
+                CK(cudaMemcpy(rowval_out, m->rows.as<int>() + b, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+            if (lower_out)
+                CK(cudaMemcpy(lower_out, m->lower.as<char>() + b * es, es * cnt, cudaMemcpyDeviceToHost));
+            if (gap_out) CK(cudaMemcpy(gap_out, m->gap.as<char>() + b * es, es * cnt, cudaMemcpyDeviceToHost));
+        }
+        return RIMDP_OK;
+    });
 }
 
 } // extern "C"

@@ -55,17 +55,19 @@ struct Ctl {
 template <class T>
 __global__ void prepare_columns(int ncols, const long long* __restrict__ colptr, const T* __restrict__ lower,
                                 T* __restrict__ upper_to_gap, T* __restrict__ rem, unsigned char* __restrict__ infeasible,
-                                T* __restrict__ quoted_sum, int* __restrict__ n_infeasible) {
+                                T* __restrict__ quoted_sum, T* __restrict__ maxgap, int* __restrict__ n_infeasible) {
     using N = Num<T>;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
         const long long b = colptr[c], e = colptr[c + 1];
-        T ls = T(0), gs = T(0);
+        T ls = T(0), gs = T(0), mg = T(0);
         for (long long i = b; i < e; ++i) {
             const T g = N::sub(upper_to_gap[i], lower[i]);
             ls = N::add(ls, lower[i]);
             gs = N::add(gs, g);
+            mg = g > mg ? g : mg;
             upper_to_gap[i] = g;
         }
+        maxgap[c] = mg;
         unsigned char bad = 0;
         T q = T(0);
         if (ls > N::add(T(1), N::tol())) {
@@ -396,6 +398,183 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
             __syncwarp();
         }
         if (lane == 0) q[c] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Sorted long columns (33 .. 8192 entries, many picks): one CTA per column.
+//
+// The column's support is sorted by the adversary ordering with a bitonic
+// network in shared memory, then the greedy assignment is evaluated in the
+// paper's cumsum form (omaximize_prefix, omax.hpp:118-138):
+// with E_j the sum of the gaps before sorted position j, position j receives
+// lower + min(gap, rem - E_j) when rem - E_j > 0 and lower otherwise.  E_j
+// comes from a block-wide prefix scan and the expectation from a block-wide
+// reduction, so every position is independent — the north_star's warp-shuffle
+// scan design.  Sums are in tree order rather than the reference's
+// sequential order: results agree within a few ulps (tests bound them by
+// 1e-12), deterministically.
+//
+// Sort key: (order key of V[row] with its low log2(N) bits dropped) | pos, a
+// unique u64 whose order is the reference's (V, row) order except among
+// entries whose keys differ only in the dropped bits; those runs are detected
+// after the sort and re-sorted exactly by the full (key, pos) (rare: values
+// within 2^-40 relative of each other).
+template <int kLogN>
+struct SortedShape {
+    static constexpr int N = 1 << kLogN;
+    static constexpr int threads = N / 4 < 32 ? 32 : (N / 4 > 512 ? 512 : N / 4);
+    static constexpr int E = N / threads; // sorted elements per thread in the scan
+    template <class T>
+    static constexpr size_t smem() { return N * (8 + sizeof(T)) + 32 * sizeof(T) + 16; }
+};
+
+template <class T, bool kPess, int kLogN>
+__global__ void __launch_bounds__(SortedShape<kLogN>::threads)
+omax_sorted(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+            const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+            const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl) {
+    using N_ = Num<T>;
+    using Bits = typename N_::Bits;
+    using Sh = SortedShape<kLogN>;
+    constexpr int N = Sh::N, NT = Sh::threads, E = Sh::E;
+    constexpr unsigned long long kPosMask = (1ull << kLogN) - 1;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    // dynamic shared memory (SortedShape::smem bytes): sort keys (later the
+    // available mass by position), gaps by position, warp partials, fix flag
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* skey = reinterpret_cast<unsigned long long*>(smem_raw);
+    T* sgap = reinterpret_cast<T*>(skey + N);
+    T* wsum = sgap + N;
+    int& fix = *reinterpret_cast<int*>(wsum + 32);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int item = blockIdx.x; item < nlist; item += gridDim.x) {
+        const int c = list[item];
+        const long long b = colptr[c];
+        const int L = static_cast<int>(colptr[c + 1] - b);
+        const T r = rem[c];
+        // load: keys and gaps by position; padding sorts last
+        for (int j = tid; j < N; j += NT) {
+            unsigned long long k = ~0ull;
+            if (j < L) {
+                const Bits full = N_::key(__ldg(V + __ldg(rows + b + j)), kPess);
+                if constexpr (sizeof(Bits) == 8)
+                    k = ((static_cast<unsigned long long>(full) >> kLogN) << kLogN) | static_cast<unsigned long long>(j);
+                else
+                    k = (static_cast<unsigned long long>(full) << kLogN) | static_cast<unsigned long long>(j);
+                sgap[j] = __ldg(gap + b + j);
+            }
+            skey[j] = k;
+        }
+        if (tid == 0) fix = 0;
+        __syncthreads();
+        // bitonic sort, ascending
+        for (int k = 2; k <= N; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < N / 2; i += NT) {
+                    const int lo = 2 * j * (i / j) + (i % j), hi = lo + j;
+                    const unsigned long long x = skey[lo], y = skey[hi];
+                    const bool up = (lo & k) == 0;
+                    if ((x > y) == up) {
+                        skey[lo] = y;
+                        skey[hi] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        if constexpr (sizeof(Bits) == 8) {
+            // exact order among entries whose truncated keys collide
+            for (int j = tid; j + 1 < L; j += NT) {
+                const unsigned long long x = skey[j], y = skey[j + 1];
+                if ((x >> kLogN) == (y >> kLogN)) {
+                    const Bits fx = N_::key(__ldg(V + __ldg(rows + b + (x & kPosMask))), kPess);
+                    const Bits fy = N_::key(__ldg(V + __ldg(rows + b + (y & kPosMask))), kPess);
+                    if (fx > fy) fix = 1;
+                }
+            }
+            __syncthreads();
+            if (fix) {
+                if (tid == 0) {
+                    // insertion sort by (full key, pos): the input is nearly sorted
+                    for (int j = 1; j < L; ++j) {
+                        const unsigned long long x = skey[j];
+                        const Bits fx = N_::key(__ldg(V + __ldg(rows + b + (x & kPosMask))), kPess);
+                        int t = j - 1;
+                        while (t >= 0) {
+                            const unsigned long long y = skey[t];
+                            const Bits fy = N_::key(__ldg(V + __ldg(rows + b + (y & kPosMask))), kPess);
+                            if (fy < fx || (fy == fx && (y & kPosMask) < (x & kPosMask))) break;
+                            skey[t + 1] = y;
+                            --t;
+                        }
+                        skey[t + 1] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // prefix scan of the gaps in sorted order: thread tid owns sorted [tid*E, tid*E+E)
+        int pos[E];
+        T g[E];
+        T run = T(0);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = tid * E + e;
+            pos[e] = j < L ? static_cast<int>(skey[j] & kPosMask) : -1;
+            g[e] = pos[e] >= 0 ? sgap[pos[e]] : T(0);
+            run = N_::add(run, g[e]);
+        }
+        // block exclusive scan of the per-thread totals
+        T incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl = N_::add(incl, y);
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads(); // also: every thread has read its keys before they are overwritten
+        if (wid == 0) {
+            T w = lane < NT / 32 ? wsum[lane] : T(0);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const T y = __shfl_up_sync(kFull, w, o);
+                if (lane >= o) w = N_::add(w, y);
+            }
+            if (lane < NT / 32) wsum[lane] = w; // inclusive warp prefix
+        }
+        __syncthreads();
+        T excl = __shfl_up_sync(kFull, incl, 1);
+        if (lane == 0) excl = T(0);
+        if (wid > 0) excl = N_::add(excl, wsum[wid - 1]);
+        // available mass at each sorted position, stored by position
+        T* avail_by_pos = reinterpret_cast<T*>(skey);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (pos[e] >= 0) avail_by_pos[pos[e]] = N_::sub(r, excl);
+            excl = N_::add(excl, g[e]);
+        }
+        __syncthreads();
+        // expectation (tree order)
+        T acc = T(0);
+        for (int j = tid; j < L; j += NT) {
+            const T a = avail_by_pos[j];
+            const T l = __ldg(lower + b + j);
+            const T gg = sgap[j];
+            const T p = a > T(0) ? N_::add(l, gg < a ? gg : a) : l;
+            acc = N_::add(acc, N_::mul(__ldg(V + __ldg(rows + b + j)), p));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = N_::add(acc, __shfl_xor_sync(kFull, acc, o));
+        __syncthreads();
+        if (lane == 0) wsum[wid] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            T t = T(0);
+            for (int w = 0; w < NT / 32; ++w) t = N_::add(t, wsum[w]);
+            q[c] = t;
+        }
+        __syncthreads();
     }
 }
 

@@ -1,7 +1,7 @@
 """ctypes binding of the C ABI in include/rimdp_b200.h.
 
 This is plumbing for tests, bench.py and the sharded driver; the drop-in
-host API for C++ callers is include/rimdp/*.hpp.  The library is loaded from
+host API for C++ callers is include/rimdp_b200/dropin.hpp.  The library is loaded from
 the package tree (``lib/librimdp_b200.so``); there is no CPU fallback — if
 the library is missing, building or loading raises.
 """
@@ -99,6 +99,7 @@ _SIGNATURES = {
     "rimdp_profile_read": ([_VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_bellman_step": ([_VP, _VP, _I32, _I32, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_column_values": ([_VP, _VP, _I32, _VP], C.c_int),
+    "rimdp_generate_host": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_random_imdp": ([_I32, _I32, _D, _D, C.c_uint64, _I32, _I32, _VP, _VP], C.c_int),
     "rimdp_random_imdp_take": ([_VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
 }
@@ -169,6 +170,42 @@ def random_imdp(states, actions, density, scale=0.2, seed=1, point=False, dtype=
     return sp, cp, rv, lo, up
 
 
+def gen_config(num_states, actions, *, law=0, support=64, alpha=1.5, kmax=4096, lower_scale=None,
+               upper_scale=None, seed=1, dtype=np.float64, device=0, state_begin=0, state_end=0) -> GenConfig:
+    """A counter-based generator configuration (csrc/generator.cuh).
+
+    law 0: `support` stratified rows per column, the reference generator's value law
+    (lower = u/k, upper = min(lower + v (1 - 1/k), 1)) by default;
+    law 1: power-law lengths k ~ k^-alpha on [1, kmax], lower = u * 0.5 / k,
+    upper = min(lower + v * 3 / k, 1) by default."""
+    if law == 0:
+        k = min(support, num_states)
+        lower_scale = 1.0 / k if lower_scale is None else lower_scale
+        upper_scale = 1.0 - 1.0 / k if upper_scale is None else upper_scale
+    else:
+        lower_scale = 0.5 if lower_scale is None else lower_scale
+        upper_scale = 3.0 if upper_scale is None else upper_scale
+    return GenConfig(_dt(dtype), device, num_states, actions, law, support, alpha, kmax, lower_scale, upper_scale,
+                     seed, state_begin, state_end)
+
+
+def generate_host(cfg: GenConfig):
+    """The generator on the host (bit-identical to rimdp_model_generate):
+    (stateptr int32, colptr int64, rowval int32, lower, upper) of the configured shard."""
+    lib = load()
+    nc, nnz = C.c_int32(), C.c_int64()
+    _check(lib.rimdp_generate_host(C.byref(cfg), C.byref(nc), C.byref(nnz), None, None, None, None, None))
+    dtype = np.float64 if cfg.dtype == RIMDP_F64 else np.float32
+    nst = (cfg.state_end - cfg.state_begin) if (cfg.state_begin or cfg.state_end) else cfg.num_states
+    sp = np.empty(nst + 1, np.int32)
+    cp = np.empty(nc.value + 1, np.int64)
+    rv = np.empty(nnz.value, np.int32)
+    lo = np.empty(nnz.value, dtype)
+    up = np.empty(nnz.value, dtype)
+    _check(lib.rimdp_generate_host(C.byref(cfg), None, None, _p(sp), _p(cp), _p(rv), _p(lo), _p(up)))
+    return sp, cp, rv, lo, up
+
+
 def _dt(dtype) -> int:
     return RIMDP_F64 if np.dtype(dtype) == np.float64 else RIMDP_F32
 
@@ -212,6 +249,17 @@ class DeviceModel:
         h = C.c_void_p()
         _check(load().rimdp_model_generate(C.byref(cfg), C.byref(h)))
         return cls(h, np.float64 if cfg.dtype == RIMDP_F64 else np.float32)
+
+    def read_columns(self, col_begin: int, col_end: int):
+        """(colptr int64 relative, rows int32, lower, gap) of columns [col_begin, col_end) as stored."""
+        cp = np.empty(col_end - col_begin + 1, np.int64)
+        _check(load().rimdp_model_read_columns(self._h, col_begin, col_end, _p(cp), None, None, None))
+        cnt = int(cp[-1])
+        rv = np.empty(cnt, np.int32)
+        lo = np.empty(cnt, self.dtype)
+        gp = np.empty(cnt, self.dtype)
+        _check(load().rimdp_model_read_columns(self._h, col_begin, col_end, _p(cp), _p(rv), _p(lo), _p(gp)))
+        return cp, rv, lo, gp
 
     def close(self):
         if getattr(self, "_h", None):
