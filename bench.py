@@ -1,16 +1,27 @@
 #!/usr/bin/env python
-"""Benchmark: transitions/s per robust Bellman iteration on BASELINE config 2.
+"""Benchmark: transitions/s per robust Bellman iteration (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference] [--config c2|c3|...]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+                    [--config c2|c3|c4|c5] [--dtype f64|f32]
 
-A "step" is one robust Bellman iteration (column O-max kernels + fused
-action/residual kernel) over the whole transition store.  `value` is
-whole-job transitions/s with the model resident in HBM (CUDA events on the
-model stream, max over ranks); `e2e` is the same metric through the public
-solve call with host buffers (model upload, plan upload, full solve to
-convergence, result download), the headline against the reference arm.
-`cpu_baseline` times the reference itself (oracle/_ref, all host threads) on
-a bounded sample of the same workload.  See DESIGN.md "Measurement".
+A "step" is one robust Bellman iteration over the whole transition store:
+the column O-max kernels, the fused action/update/residual kernel and, at
+N > 1, the value all-gather + residual all-reduce of the state-sharded
+solve.  The default workload is BASELINE config 2 (configs[1], the one the
+metric is quoted on that fits one GPU).
+
+  value     whole-job transitions/s, model resident in HBM, CUDA events on the
+            model stream around exactly K steps (max over ranks at N > 1)
+  e2e       the same metric through the public solve call with host buffers:
+            model upload (host-generated configs) + plan upload + solve to
+            convergence + result download, divided over the iterations
+  roofline  the column phase (the dominant kernels) against HBM: algorithmic
+            bytes = transitions x (index + lower + gap + V gather) per launch
+             / its event-timed duration
+  cpu_baseline  the reference itself (oracle/_ref, all host threads) on a
+            bounded sample of the same workload (rank 0, N = 1)
+
+See DESIGN.md "Measurement".
 """
 from __future__ import annotations
 
@@ -29,15 +40,27 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # SURVEY §8(d) synthetic inputs; the generator is the reference's own law
+    # SURVEY §8(d) synthetic inputs
     "c2": dict(desc="C2: random_imdp 100000 states x 4 actions x 32 successors (12.8M transitions), "
-                    "Pmaxmin InfiniteTimeReachability(goal = last 1% of states, eps = 1e-6), f64",
-               states=100000, actions=4, density=32.0 / 100000, scale=1.0 / 32, seed=1, goal_frac=0.01,
-               pessimistic=True, maximize=True, eps=1e-6),
+                    "Pmaxmin InfiniteTimeReachability(goal = last 1% of states, eps = 1e-6)",
+               source="reference", states=100000, actions=4, density=32.0 / 100000, scale=1.0 / 32, seed=1,
+               kind="reach", goal_frac=0.01, pessimistic=True, maximize=True, eps=1e-6,
+               sample=None),
     "c3": dict(desc="C3: random_imdp 2000 states x 10 actions x 2000 successors (40M transitions), "
-                    "Pminmin InfiniteTimeReachability(goal = last 1%, eps = 1e-6), f64",
-               states=2000, actions=10, density=1.0, scale=1.0 / 2000, seed=1, goal_frac=0.01,
-               pessimistic=True, maximize=False, eps=1e-6),
+                    "Pminmin InfiniteTimeReachability(goal = last 1%, eps = 1e-6), long-column path",
+               source="reference", states=2000, actions=10, density=1.0, scale=1.0 / 2000, seed=1,
+               kind="reach", goal_frac=0.01, pessimistic=True, maximize=False, eps=1e-6, sample=None),
+    "c4": dict(desc="C4: 10M states x 8 actions x 64 successors (5.12e9 transitions, counter-based generator "
+                    "in HBM), Pmaxmin InfiniteTimeReachability(goal = last 1%, eps = 1e-6)",
+               source="generated", states=10_000_000, actions=8, law=0, support=64, seed=1,
+               kind="reach", goal_frac=0.01, pessimistic=True, maximize=True, eps=1e-6,
+               sample=dict(states=100_000)),
+    "c5": dict(desc="C5: 1M states x 4 actions, power-law successor counts k^-1.5 on [1, 4096] (~2e8 "
+                    "transitions, generated in HBM), discounted reward gamma = 0.95, Pmax strategy synthesis, "
+                    "eps = 1e-6",
+               source="generated", states=1_000_000, actions=4, law=1, alpha=1.5, kmax=4096, seed=1,
+               kind="reward", discount=0.95, pessimistic=True, maximize=True, eps=1e-6,
+               sample=dict(states=50_000)),
 }
 
 
@@ -50,14 +73,13 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+        return float(d["hbm_gbs"]), "of measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "of fallback (B200_PROFILING.md 6.65 TB/s; MEASURED_PEAKS.json absent)"
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons, sampled every 20 ms from before the
-    timed region until after the last GPU phase (timed region, kernel-timing
-    pass and the end-to-end solve): every sample after the "timed" mark is
+    """nvidia-smi clocks and throttle reasons every 20 ms from before the timed
+    region until after the last GPU phase; samples after the "timed" mark are
     taken under load."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -119,67 +141,154 @@ class ClockSampler:
                 "window": "timed region through kernel-timing pass and end-to-end solve (GPU busy)"}
 
 
-def make_problem(w):
+# ---------------------------------------------------------------------------
+# workloads
+
+def goal_states(n, frac):
+    return np.arange(n - int(round(n * frac)), n)
+
+
+def rewards_for(n, seed):
+    return np.random.default_rng(seed).random(n)
+
+
+def gen_cfg(w, dtype, states=None, device=0, state_begin=0, state_end=0):
+    from paper_2401_04068_b200 import engine
+    return engine.gen_config(states or w["states"], w["actions"], law=w["law"], support=w.get("support", 64),
+                             alpha=w.get("alpha", 1.5), kmax=w.get("kmax", 4096), seed=w["seed"], dtype=dtype,
+                             device=device, state_begin=state_begin, state_end=state_end)
+
+
+def host_arrays(w, dtype, states=None):
+    """Host CSC arrays of the workload (or of its down-scaled CPU sample)."""
+    from paper_2401_04068_b200 import engine
+    if w["source"] == "reference":
+        return engine.random_imdp(states or w["states"], w["actions"], w["density"], w["scale"], w["seed"],
+                                  dtype=dtype)
+    return engine.generate_host(gen_cfg(w, dtype, states=states))
+
+
+def plan_kw(w, n, dtype):
+    """The marshalled plan (solver.hpp:40-80) of the workload's specification."""
+    dt = np.dtype(dtype)
+    if w["kind"] == "reach":
+        frozen = np.zeros(n, np.uint8)
+        frozen[goal_states(n, w["goal_frac"])] = 1
+        return dict(initial=frozen.astype(dt), frozen=frozen, pessimistic=w["pessimistic"], maximize=w["maximize"],
+                    eps=float(dt.type(w["eps"])))
+    r = rewards_for(n, w["seed"]).astype(dt)
+    return dict(initial=r, rewards=r, discount=float(dt.type(w["discount"])), pessimistic=w["pessimistic"],
+                maximize=w["maximize"], eps=float(dt.type(w["eps"])))
+
+
+def spec_for(w, n, dtype):
+    from paper_2401_04068_b200 import problems as P
+    sat = P.PESSIMISTIC if w["pessimistic"] else P.OPTIMISTIC
+    strat = P.MAXIMIZE if w["maximize"] else P.MINIMIZE
+    if w["kind"] == "reach":
+        return P.Specification(P.InfiniteTimeReachability(list(goal_states(n, w["goal_frac"])), w["eps"]), sat, strat)
+    return P.Specification(P.InfiniteTimeReward(rewards_for(n, w["seed"]).astype(dtype), w["discount"], w["eps"]),
+                           sat, strat)
+
+
+# ---------------------------------------------------------------------------
+# engine arm
+
+def build_model(w, dtype, rank, world, local):
+    """This rank's store: the whole model (N = 1) or its state shard."""
+    from paper_2401_04068_b200 import engine, sharded
     n = w["states"]
-    goal = list(range(n - int(round(n * w["goal_frac"])), n))
-    return goal
+    sb, se = sharded.shard_ranges(n, world)[rank]
+    t0 = time.time()
+    arrays = None
+    if w["source"] == "reference":
+        arrays = host_arrays(w, dtype)
+        if world == 1:
+            m = engine.DeviceModel.from_csc(*arrays, device=local)
+        else:
+            m = engine.DeviceModel.from_csc_shard(*sharded.slice_csc(*arrays, sb, se), sb, n, device=local)
+    else:
+        cfg = gen_cfg(w, dtype, device=local, state_begin=sb if world > 1 else 0, state_end=se if world > 1 else 0)
+        m = engine.DeviceModel.generate(cfg)
+    log(f"[bench] rank {rank}: states [{sb}, {se}), {m.nnz} transitions built in {time.time() - t0:.1f}s")
+    return m, arrays
 
 
 def engine_arm(args, w):
     import torch
-    from paper_2401_04068_b200 import engine, problems as P
+    from paper_2401_04068_b200 import engine, problems as P, sharded
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    t0 = time.time()
-    arrays = engine.random_imdp(w["states"], w["actions"], w["density"], w["scale"], w["seed"])
-    sp, cp, rv, lo, up = arrays
-    nnz = int(cp[-1])
-    log(f"[bench] generated {w['states']} states, {nnz} transitions in {time.time() - t0:.1f}s")
-    goal = make_problem(w)
+    dtype = np.float64 if args.dtype == "f64" else np.float32
+    es = np.dtype(dtype).itemsize
     n = w["states"]
-    spec = P.Specification(P.InfiniteTimeReachability(goal, w["eps"]),
-                           P.PESSIMISTIC if w["pessimistic"] else P.OPTIMISTIC,
-                           P.MAXIMIZE if w["maximize"] else P.MINIMIZE)
-    plan = P.make_plan(spec, n, np.float64)
+    m, arrays = build_model(w, dtype, rank, world, local)
+    local_nnz = m.nnz
+    total_nnz = local_nnz
+    if world > 1:
+        t = torch.tensor([local_nnz, local_nnz], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t[:1], op=dist.ReduceOp.SUM)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
+        total_nnz, max_nnz = int(t[0]), int(t[1])
+    kw = plan_kw(w, n, dtype)
+    total = args.warmup + args.steps
+    run_kw = dict(kw, finite=True, horizon=total + 1)  # a fixed number of iterations: no early stop
+    stream = torch.cuda.ExternalStream(m.stream(), device=torch.device("cuda", local))
+    clk = ClockSampler(local).__enter__()
+    time.sleep(0.3)
 
     # ---- resident throughput (value) ------------------------------------
-    m = engine.DeviceModel.from_csc(sp, cp, rv, lo, up, device=local)
-    stream = torch.cuda.ExternalStream(m.stream(), device=torch.device("cuda", local))
-    total = args.warmup + args.steps
-    kw = dict(initial=plan.initial, frozen=plan.frozen, finite=True, horizon=total + 1,
-              pessimistic=w["pessimistic"], maximize=w["maximize"])
-    clk = ClockSampler(local).__enter__()  # sampled through every GPU phase below
-    time.sleep(0.3)  # let nvidia-smi start sampling before the GPU work begins
-    m.begin(**kw)
-    m.advance(args.warmup)
-    m.poll()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    clk.mark("timed")
-    start.record(stream)
-    m.advance(args.steps)
-    end.record(stream)
-    torch.cuda.synchronize()
+    if world == 1:
+        m.begin(**run_kw)
+        m.advance(args.warmup)
+        m.poll()
+        torch.cuda.synchronize()
+        clk.mark("timed")
+        start.record(stream)
+        m.advance(args.steps)
+        end.record(stream)
+        torch.cuda.synchronize()
+        k_done, _, _ = m.poll()
+        assert k_done == total, (k_done, total)
+    else:
+        shard = sharded.DeviceShard(m, rank, world, n)
+        solver = sharded.ShardedSolver(shard)
+        shard.begin(**run_kw)
+        with shard.stream_context():
+            for k in range(1, args.warmup + 1):
+                solver.enqueue(k)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark("timed")
+        with shard.stream_context():
+            start.record(stream)
+            for k in range(args.warmup + 1, total + 1):
+                solver.enqueue(k)
+            end.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        k_done, _, _ = shard.poll()
+        assert k_done == total, (k_done, total)
+        m.finish()
     clk.mark("end")
     ms = start.elapsed_time(end)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    k_done, _, _ = m.poll()
-    assert k_done == total, (k_done, total)
     ms_per_step = ms / args.steps
 
-    # ---- dominant kernel timing (separate pass, events per launch) ------
-    m.begin(**kw)
+    # ---- dominant kernels: the column phase, event-timed per launch ------
+    m.begin(**run_kw)
     m.advance(args.warmup)
     m.poll()
     m.profile(True)
@@ -190,67 +299,88 @@ def engine_arm(args, w):
     m.profile(False)
     m.finish()
     fused_avg, cols_avg, act_avg = fused_ms / it, cols_ms / it, act_ms / it
+    info = m.info()
     if fused_avg >= cols_avg:
         kernel_name, kernel_avg = "bellman_short (fused column O-max + action + residual)", fused_avg
     else:
-        kernel_name, kernel_avg = "omax_long/omax_short (per-column O-max of long states)", cols_avg
-    es = 8
-    alg_bytes = nnz * (4 + es + es + es)  # index + lower + gap + V gather
+        kernel_name, kernel_avg = "column O-max phase (omax_short / omax_long / omax_sorted launches)", cols_avg
+    alg_bytes = local_nnz * (4 + es + es + es)  # index + lower + gap + V gather
     peak, peak_src = load_peaks()
     achieved = alg_bytes / (kernel_avg * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         with open(tf) as f:
-            traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
-    info = m.info()
-    m.close()
+            traffic = json.load(f).get(f"{args.config}_{args.dtype}", {}).get("dram_bytes_per_launch")
 
     # ---- end to end through the public API with host buffers ------------
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t = time.perf_counter()
-    dm = engine.DeviceModel.from_csc(sp, cp, rv, lo, up, device=local)
-    vf = P.value_iteration(dm, spec)
+    h2d = sum(np.asarray(v).nbytes for v in kw.values() if isinstance(v, np.ndarray))
+    if world == 1:
+        if arrays is not None:
+            dm = engine.DeviceModel.from_csc(*arrays, device=local)
+            h2d += sum(a.nbytes for a in arrays)
+        else:
+            dm = m
+        vf = P.value_iteration(dm, spec_for(w, n, dtype))
+        e2e_iters, values, residual = vf.iterations, vf.values, vf.residual
+    else:
+        if arrays is not None:
+            parts = sharded.slice_csc(*arrays, *sharded.shard_ranges(n, world)[rank])
+            dm = engine.DeviceModel.from_csc_shard(*parts, sharded.shard_ranges(n, world)[rank][0], n, device=local)
+            h2d += sum(a.nbytes for a in parts)
+        else:
+            dm = m
+        res = sharded.ShardedSolver(sharded.DeviceShard(dm, rank, world, n)).solve(finite=False, **kw)
+        e2e_iters, values, residual = res.iterations, res.values, res.residual
     e2e_s = time.perf_counter() - t
-    dm.close()
-    h2d = sp.nbytes + cp.nbytes + rv.nbytes + lo.nbytes + up.nbytes + plan.initial.nbytes + plan.frozen.nbytes
-    d2h = vf.values.nbytes + vf.residual.nbytes
-    e2e_iters = vf.iterations
-    ref_iters = None
-    bit_exact = None
+    if world > 1:
+        tt = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    d2h = values.nbytes + residual.nbytes
+    ref_iters = bit_exact = None
     gj = os.path.join(ROOT, "tests", "golden", f"{args.config}.json")
-    if os.path.exists(gj):
+    if os.path.exists(gj) and args.dtype == "f64":
         import hashlib
         with open(gj) as f:
             run = json.load(f)["runs"].get(f"m{int(w['maximize'])}p{int(w['pessimistic'])}")
         if run:
             ref_iters = run["iterations"]
-            bit_exact = (hashlib.sha256(vf.values.tobytes()).hexdigest() == run["values_sha256"] and
-                         hashlib.sha256(vf.residual.tobytes()).hexdigest() == run["residual_sha256"])
-
+            bit_exact = (hashlib.sha256(values.tobytes()).hexdigest() == run["values_sha256"] and
+                         hashlib.sha256(residual.tobytes()).hexdigest() == run["residual_sha256"])
+    m.close()
     clk.__exit__()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_sample(arrays, w, plan, budget_s=args.cpu_budget)
+        cpu = cpu_sample(w, dtype, budget_s=args.cpu_budget)
 
-    clocks = clk.summary()
     out = {
         "metric": "transitions/sec per Bellman iteration",
-        "value": nnz * world / (ms_per_step * 1e-3),
+        "value": total_nnz / (ms_per_step * 1e-3),
         "unit": "transitions/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (reference random_imdp law, seed 1; generated on host, resident in HBM)",
-        "config": {"workload": w["desc"], "states": n, "columns": int(len(cp) - 1), "transitions": nnz,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "per-iteration inputs (28 B x transitions) exceed the 126 MB L2; no flush needed",
-                   "scheduler": {"short_columns": info.short_columns, "long_columns": info.long_columns}},
+        "dtype": args.dtype,
+        "data": ("synthetic (reference random_imdp law, seed 1; generated on host, resident in HBM)"
+                 if w["source"] == "reference" else
+                 "synthetic (counter-based generator, seed 1, generated directly in HBM)"),
+        "config": {"workload": w["desc"], "states": n, "columns": n * w["actions"], "transitions": total_nnz,
+                   "parallelism": f"state-sharded x{world} (NCCL all-gather of V)" if world > 1 else "single GPU",
+                   "l2": ("per-iteration inputs (index + bounds, 20 B x transitions) exceed the 126 MB L2; "
+                          "no flush needed" if total_nnz * (4 + 2 * es) > 126e6 else
+                          "inputs fit in L2 (reported as is)"),
+                   "scheduler": {"short_columns": info.short_columns, "exact_long_columns": info.mid_columns,
+                                 "sorted_long_columns": info.long_columns, "max_column_length":
+                                 info.max_column_length}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": kernel_name,
                      "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": kernel_avg,
@@ -258,46 +388,59 @@ def engine_arm(args, w):
                                   "action_kernel": act_avg},
                      "kernel_share_of_step": kernel_avg / max(fused_avg + cols_avg + act_avg, 1e-12),
                      "peak_source": peak_src},
-        "e2e": {"value": nnz * e2e_iters / e2e_s, "unit": "transitions/s", "h2d_bytes_per_step": h2d / e2e_iters,
-                "d2h_bytes_per_step": d2h / e2e_iters, "seconds_to_convergence": e2e_s, "iterations": e2e_iters,
-                "reference_iterations": ref_iters, "values_bit_exact_vs_reference": bit_exact, "call": "DeviceModel.from_csc + problems.value_iteration (C ABI)"},
+        "e2e": {"value": total_nnz * e2e_iters / e2e_s, "unit": "transitions/s",
+                "h2d_bytes_per_step": h2d / max(e2e_iters, 1), "d2h_bytes_per_step": d2h / max(e2e_iters, 1),
+                "seconds_to_convergence": e2e_s, "iterations": e2e_iters,
+                "reference_iterations": ref_iters, "values_bit_exact_vs_reference": bit_exact,
+                "call": ("DeviceModel.from_csc + problems.value_iteration (C ABI)" if world == 1 else
+                         "DeviceModel.from_csc_shard + sharded.ShardedSolver.solve (C ABI + NCCL)")},
         "time_to_convergence_s": e2e_s,
-        "gpu_launches": args.steps * kpi,
-        "clocks": clocks,
+        "gpu_launches": args.steps * (kpi + (1 if world > 1 else 0)),
+        "clocks": clk.summary(),
     }
+    if world > 1:
+        out["config"]["shard_nnz_max_over_mean"] = max_nnz / (total_nnz / world)
+        out["scaling"] = "strong"
     if cpu:
         out["cpu_baseline"] = cpu
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
-        torch.distributed.destroy_process_group()
+        dist.destroy_process_group()
 
+
+# ---------------------------------------------------------------------------
+# CPU reference (the checker, timed)
 
 _CPU_MODELS: dict = {}
 
 
-def cpu_sample(arrays, w, plan, budget_s=15.0, which=None, model_cache=True):
-    """The reference (oracle/_ref, all host threads) on a bounded number of
-    iterations of the same workload; the oracle port (1 thread) if the
-    reference library is absent."""
+def cpu_sample(w, dtype, budget_s=15.0, which=None):
+    """The reference (oracle/_ref, all host threads; the oracle port on 1 thread
+    if the reference library is absent) on a bounded number of iterations of
+    the workload (configs 4-5: of its law at the `sample` state count)."""
     import oracle
-    sp, cp, rv, lo, up = arrays
     which = which or ("ref" if oracle.ref_available() else "port")
     if which == "port" and not oracle.port_available():
         oracle.build(ref=False)
     cores = os.cpu_count() if which == "ref" else 1
-    key = (which, id(arrays))
-    m = _CPU_MODELS.get(key) if model_cache else None
-    if m is None:
+    states = (w.get("sample") or {}).get("states")
+    key = (which, w["desc"], np.dtype(dtype).str)
+    if key not in _CPU_MODELS:
         t = time.time()
-        m = oracle.Model.from_arrays(which, sp, cp, rv, lo, up)
+        arrays = host_arrays(w, dtype, states=states)
+        _CPU_MODELS[key] = (oracle.Model.from_arrays(which, *arrays), int(arrays[1][-1]), len(arrays[0]) - 1)
         log(f"[bench] cpu model ({which}) built in {time.time() - t:.1f}s")
-        _CPU_MODELS[key] = m
-    goal = np.nonzero(plan.frozen)[0].tolist()
+    m, nnz, n = _CPU_MODELS[key]
+    kw = plan_kw(w, n, dtype)
 
     def run(k):
-        pr = oracle.Problem(oracle.FINITE_REACH, reach=goal, horizon=k, pessimistic=w["pessimistic"],
-                            maximize=w["maximize"])
+        if w["kind"] == "reach":
+            pr = oracle.Problem(oracle.FINITE_REACH, reach=list(np.nonzero(kw["frozen"])[0]), horizon=k,
+                                pessimistic=w["pessimistic"], maximize=w["maximize"])
+        else:
+            pr = oracle.Problem(oracle.FINITE_REWARD, rewards=kw["rewards"], discount=kw["discount"], horizon=k,
+                                pessimistic=w["pessimistic"], maximize=w["maximize"])
         t0 = time.perf_counter()
         m.solve(pr, workers=0)
         return time.perf_counter() - t0
@@ -305,40 +448,39 @@ def cpu_sample(arrays, w, plan, budget_s=15.0, which=None, model_cache=True):
     one = run(1)
     k = max(1, min(200, int(budget_s / max(one, 1e-6))))
     secs = run(k)
-    nnz = int(cp[-1])
+    scope = "the same workload" if not states else f"the same law at {n} states ({nnz} transitions)"
     return {"value": nnz * k / secs, "unit": "transitions/s", "cores": cores,
             "kind": "reference" if which == "ref" else "port",
-            "sample": f"{k} Bellman iterations of the same workload (FiniteTimeReachability horizon {k}, "
-                      f"same goal set and modes), value_iteration with workers=0, {secs:.2f}s"}
+            "sample": f"{k} Bellman iterations of {scope} (finite-horizon {k}, same goal/reward and modes), "
+                      f"value_iteration with workers=0, {secs:.2f}s"}
 
 
 def reference_arm(args, w):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2401_04068_b200 import engine
-    arrays = engine.random_imdp(w["states"], w["actions"], w["density"], w["scale"], w["seed"])
-    from paper_2401_04068_b200 import problems as P
-    goal = make_problem(w)
-    spec = P.Specification(P.InfiniteTimeReachability(goal, w["eps"]))
-    plan = P.make_plan(spec, w["states"], np.float64)
+    dtype = np.float64 if args.dtype == "f64" else np.float32
     target = min(3.0, 120.0 / max(1, args.steps))
     cpu = None
-    for _ in range(args.warmup and 1):
-        cpu = cpu_sample(arrays, w, plan, budget_s=target)
+    for _ in range(1 if args.warmup else 0):
+        cpu = cpu_sample(w, dtype, budget_s=target)
     vals = []
     for _ in range(args.steps):
-        cpu = cpu_sample(arrays, w, plan, budget_s=target, model_cache=True)
+        cpu = cpu_sample(w, dtype, budget_s=target)
         vals.append(cpu["value"])
     v = statistics.median(vals)
-    nnz = int(arrays[1][-1])
+    nnz_full = None
+    if w["source"] == "reference":
+        from paper_2401_04068_b200 import engine
+        nnz_full = int(engine.random_imdp(w["states"], w["actions"], w["density"], w["scale"], w["seed"])[1][-1])
     cpu["value"] = v
     out = {"impl": "reference", "metric": "transitions/sec per Bellman iteration", "value": v,
            "unit": "transitions/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": nnz / v * 1e3, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference random_imdp law, seed 1)",
-           "config": {"workload": w["desc"], "states": w["states"], "transitions": nnz,
-                      "parallelism": "host threads"},
+           "warmup": args.warmup, "ms_per_step": (nnz_full / v * 1e3) if nnz_full else None,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+           "data": "synthetic (same generator and seed as the engine arm)",
+           "config": {"workload": w["desc"], "states": w["states"], "transitions": nnz_full,
+                      "parallelism": f"host threads ({os.cpu_count()})"},
            "cpu_baseline": cpu,
            "e2e": {"value": v, "unit": "transitions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -351,6 +493,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define RIMDP_B200_ABI_VERSION 1
+#define RIMDP_B200_ABI_VERSION 2
 
 /* Scalar type of a model: NumericTraits<double|float> (numeric.hpp:53-81).
  * The exact Rational instantiation (numeric.hpp:83-101) has no device path. */
@@ -85,6 +85,16 @@ typedef struct rimdp_model_desc {
 } rimdp_model_desc;
 
 int rimdp_model_create(const rimdp_model_desc* desc, rimdp_model** out);
+/* One shard of a model for state-sharded multi-GPU solves: `desc` holds the
+ * local states [state_begin, state_begin + desc->num_states) only (stateptr
+ * and colptr local, rows global destinations in [0, num_global_states)).
+ * The value vector stays global: V is replicated on every shard. */
+int rimdp_model_create_shard(const rimdp_model_desc* desc, int32_t state_begin, int32_t num_global_states,
+                             rimdp_model** out);
+/* Capacity (entries) of the solve's value buffers, >= the global state
+ * count: the sharded driver pads V to world_size equal slices so one
+ * in-place all-gather per iteration can exchange it. */
+int rimdp_model_set_value_capacity(rimdp_model* model, int64_t entries);
 int rimdp_model_destroy(rimdp_model* model);
 
 /* Synthetic transition stores generated directly in HBM by a counter-based
@@ -154,6 +164,7 @@ typedef struct rimdp_plan {
     double discount;          /* converted to dtype */
     const int32_t* forced;    /* NULL, [n] (stationary) or [horizon][n] (row t = horizon - k) */
     int32_t forced_time_dependent;
+    int32_t external_stop;    /* sharded solves: the device stop test waits for rimdp_solve_stop_test */
 } rimdp_plan;
 
 /* Called after iteration k with V_k on the host (on_iteration_f64,
@@ -194,6 +205,14 @@ int rimdp_profile_read(rimdp_model* model, double* fused_ms, double* columns_ms,
 /* Device pointers of the solve's double-buffered value vector, for
  * collective exchange in the sharded driver: V_k lives in buffer k & 1. */
 int rimdp_solve_value_buffers(rimdp_model* model, void** buf0, void** buf1);
+/* Device pointer to the two per-iteration residual slots (uint64 bit patterns
+ * of the non-negative max residual; iteration k uses slot k & 1).  With
+ * external_stop, the driver max-reduces slot k & 1 across shards after
+ * iteration k and then calls rimdp_solve_stop_test. */
+int rimdp_solve_residual_slots(rimdp_model* model, void** slots);
+/* Enqueues the stop test of the last enqueued iteration on the model stream
+ * (solver.hpp:127-134 with the residual now global). */
+int rimdp_solve_stop_test(rimdp_model* model);
 
 /* One Bellman step from `v_in` (bellman.hpp:127-133, with the optional
  * forced column per state of bellman_step_impl, :96-101). */

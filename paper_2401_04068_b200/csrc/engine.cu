@@ -130,6 +130,7 @@ struct rimdp_model {
     cudaStream_t stream = nullptr;
     int n = 0;         // states owned by this store (local)
     int n_global = 0;  // length of the value vector
+    long long value_capacity = 0; // allocated entries of the value buffers (>= n_global)
     int state_begin = 0;
     int ncols = 0;
     long long nnz = 0;
@@ -371,8 +372,13 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     s.max_iterations = p->max_iterations;
     s.eps = p->eps;
     s.discount = p->discount;
-    s.v[0].ensure(sizeof(T) * N);
-    s.v[1].ensure(sizeof(T) * N);
+    const long long cap = std::max<long long>(N, m->value_capacity);
+    s.v[0].ensure(sizeof(T) * cap);
+    s.v[1].ensure(sizeof(T) * cap);
+    if (cap > N) {
+        CK(cudaMemsetAsync(s.v[0].as<T>() + N, 0, sizeof(T) * (cap - N), m->stream));
+        CK(cudaMemsetAsync(s.v[1].as<T>() + N, 0, sizeof(T) * (cap - N), m->stream));
+    }
     s.q.ensure(sizeof(T) * std::max(1, m->ncols));
     s.res.ensure(sizeof(T) * N);
     s.ctl.ensure(sizeof(Ctl));
@@ -411,6 +417,7 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     CK(cudaMemsetAsync(s.work.p, 0, 2 * kWorkKinds * sizeof(unsigned), m->stream));
     s.launched = 0;
     s.active = true;
+    s.record_only = p->external_stop != 0;
 }
 
 template <class T, bool P, int LG>
@@ -766,7 +773,22 @@ int rimdp_device_count(int* count) {
     return RIMDP_OK;
 }
 
+static int model_create_impl(const rimdp_model_desc* d, int state_begin, int num_global, rimdp_model** out);
+
 int rimdp_model_create(const rimdp_model_desc* d, rimdp_model** out) {
+    if (!d) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    return model_create_impl(d, 0, d->num_states, out);
+}
+
+int rimdp_model_create_shard(const rimdp_model_desc* d, int32_t state_begin, int32_t num_global, rimdp_model** out) {
+    if (!d) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    if (state_begin < 0 || num_global < 0 || (long long)state_begin + d->num_states > num_global)
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "shard [%d, %lld) outside [0, %d)", state_begin,
+                    (long long)state_begin + d->num_states, num_global);
+    return model_create_impl(d, state_begin, num_global, out);
+}
+
+static int model_create_impl(const rimdp_model_desc* d, int state_begin, int num_global, rimdp_model** out) {
     return guarded([&]() -> int {
         if (!d || !out) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
         if (d->dtype != RIMDP_F64 && d->dtype != RIMDP_F32) return fail(RIMDP_ERR_INVALID_ARGUMENT, "unknown dtype");
@@ -788,7 +810,9 @@ int rimdp_model_create(const rimdp_model_desc* d, rimdp_model** out) {
         m->dtype = d->dtype;
         init_common(m.get(), d->device);
         DeviceGuard g(m->device);
-        m->n = m->n_global = d->num_states;
+        m->n = d->num_states;
+        m->n_global = num_global;
+        m->state_begin = state_begin;
         m->ncols = d->num_cols;
         m->nnz = d->nnz;
         m->h_stateptr.assign(d->stateptr, d->stateptr + d->num_states + 1);
@@ -964,6 +988,35 @@ int rimdp_profile_read(rimdp_model* m, double* fused_ms, double* columns_ms, dou
         if (kernels) *kernels = kernels_per_iteration(m);
         return RIMDP_OK;
     });
+}
+
+int rimdp_solve_residual_slots(rimdp_model* m, void** slots) {
+    if (!m || !m->s.active || !slots) return fail(RIMDP_ERR_INVALID_ARGUMENT, "no active solve");
+    *slots = m->s.ctl.as<Ctl>()->res_bits;
+    return RIMDP_OK;
+}
+
+int rimdp_solve_stop_test(rimdp_model* m) {
+    if (!m || !m->s.active) return fail(RIMDP_ERR_INVALID_ARGUMENT, "no active solve");
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        SolveState& s = m->s;
+        if (s.launched == 0) return RIMDP_OK;
+        if (m->dtype == RIMDP_F64)
+            stop_test<double><<<1, 1, 0, m->stream>>>(s.ctl.as<Ctl>(), s.launched, s.finite, s.horizon,
+                                                      s.max_iterations, (double)s.eps);
+        else
+            stop_test<float><<<1, 1, 0, m->stream>>>(s.ctl.as<Ctl>(), s.launched, s.finite, s.horizon,
+                                                     s.max_iterations, (float)s.eps);
+        CK(cudaGetLastError());
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_model_set_value_capacity(rimdp_model* m, int64_t entries) {
+    if (!m || entries < 0) return fail(RIMDP_ERR_INVALID_ARGUMENT, "bad argument");
+    m->value_capacity = entries;
+    return RIMDP_OK;
 }
 
 int rimdp_solve_value_buffers(rimdp_model* m, void** b0, void** b1) {

@@ -953,6 +953,24 @@ bellman_short(int nbatch, const int* __restrict__ slots, const int2* __restrict_
     warp_epilogue<T>(myres, a, eps, ctl, &s_res, &s_arrived);
 }
 
+// Stop test of a sharded iteration k after the residual slot holds the
+// max over all shards (external_stop; solver.hpp:127-134).
+template <class T>
+__global__ void stop_test(Ctl* ctl, long long k, int finite, long long horizon, long long max_iterations, T eps) {
+    using N = Num<T>;
+    if (ctl->done) return;
+    const T res = N::from_res_bits(ctl->res_bits[k & 1]);
+    ctl->res_last = static_cast<double>(res);
+    if (finite) {
+        if (k >= horizon) ctl->done = 1;
+    } else if (res <= eps) {
+        ctl->done = 1;
+    } else if (k >= max_iterations) {
+        ctl->done = 1;
+        ctl->status = 1;
+    }
+}
+
 template <class T>
 __global__ void residual_vector(int n, const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out) {
     using N = Num<T>;

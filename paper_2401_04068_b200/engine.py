@@ -61,7 +61,7 @@ class Plan(C.Structure):
     _fields_ = [("pessimistic", C.c_int32), ("maximize", C.c_int32), ("finite", C.c_int32), ("horizon", C.c_int64),
                 ("eps", C.c_double), ("max_iterations", C.c_int64), ("initial", C.c_void_p), ("frozen", C.c_void_p),
                 ("rewards", C.c_void_p), ("discount", C.c_double), ("forced", C.c_void_p),
-                ("forced_time_dependent", C.c_int32)]
+                ("forced_time_dependent", C.c_int32), ("external_stop", C.c_int32)]
 
 
 ITER_CB = C.CFUNCTYPE(None, C.c_int64, C.c_void_p, C.c_void_p)
@@ -85,6 +85,10 @@ _SIGNATURES = {
     "rimdp_device_count": ([_VP], C.c_int),
     "rimdp_model_create": ([_VP, _VP], C.c_int),
     "rimdp_model_destroy": ([_VP], C.c_int),
+    "rimdp_model_create_shard": ([_VP, _I32, _I32, _VP], C.c_int),
+    "rimdp_model_set_value_capacity": ([_VP, _I64], C.c_int),
+    "rimdp_solve_residual_slots": ([_VP, _VP], C.c_int),
+    "rimdp_solve_stop_test": ([_VP], C.c_int),
     "rimdp_model_generate": ([_VP, _VP], C.c_int),
     "rimdp_model_read_columns": ([_VP, _I32, _I32, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_model_info_get": ([_VP, _VP], C.c_int),
@@ -245,6 +249,22 @@ class DeviceModel:
         return cls(h, dtype)
 
     @classmethod
+    def from_csc_shard(cls, stateptr, colptr, rowval, lower, upper, state_begin: int, num_global_states: int,
+                       device: int = 0) -> "DeviceModel":
+        """One shard: local stateptr/colptr (rebased to 0), global destination rows."""
+        lower = np.asarray(lower)
+        dtype = lower.dtype
+        sp = np.ascontiguousarray(stateptr, np.int32)
+        cp = np.ascontiguousarray(colptr, np.int64)
+        rv = np.ascontiguousarray(rowval, np.int32)
+        lo = np.ascontiguousarray(lower, dtype)
+        up = np.ascontiguousarray(upper, dtype)
+        d = ModelDesc(_dt(dtype), device, len(sp) - 1, len(cp) - 1, int(cp[-1]), _p(sp), _p(cp), _p(rv), _p(lo), _p(up))
+        h = C.c_void_p()
+        _check(load().rimdp_model_create_shard(C.byref(d), int(state_begin), int(num_global_states), C.byref(h)))
+        return cls(h, dtype)
+
+    @classmethod
     def generate(cls, cfg: GenConfig) -> "DeviceModel":
         h = C.c_void_p()
         _check(load().rimdp_model_generate(C.byref(cfg), C.byref(h)))
@@ -284,7 +304,7 @@ class DeviceModel:
 
     # -- plans ---------------------------------------------------------------
     def _plan(self, *, initial, pessimistic=True, maximize=True, finite=True, horizon=0, eps=0.0,
-              max_iterations=1_000_000, frozen=None, rewards=None, discount=0.0, forced=None):
+              max_iterations=1_000_000, frozen=None, rewards=None, discount=0.0, forced=None, external_stop=False):
         keep = []
         n = self.num_states if self.state_end - self.state_begin == self.num_states else None
         v0 = np.ascontiguousarray(initial, self.dtype)
@@ -296,7 +316,7 @@ class DeviceModel:
         del n
         plan = Plan(int(bool(pessimistic)), int(bool(maximize)), int(bool(finite)), int(horizon), float(eps),
                     int(max_iterations), _p(v0), _p(fz), _p(rw), float(discount), _p(fc),
-                    int(fc is not None and fc.ndim == 2))
+                    int(fc is not None and fc.ndim == 2), int(bool(external_stop)))
         return plan, keep
 
     def solve(self, *, record="none", on_iteration=None, **kw):
@@ -377,6 +397,17 @@ class DeviceModel:
         f, c, a, it, kp = C.c_double(), C.c_double(), C.c_double(), C.c_int64(), C.c_int32()
         _check(load().rimdp_profile_read(self._h, C.byref(f), C.byref(c), C.byref(a), C.byref(it), C.byref(kp)))
         return f.value, c.value, a.value, it.value, kp.value
+
+    def set_value_capacity(self, entries: int):
+        _check(load().rimdp_model_set_value_capacity(self._h, int(entries)))
+
+    def residual_slots(self) -> int:
+        p = C.c_void_p()
+        _check(load().rimdp_solve_residual_slots(self._h, C.byref(p)))
+        return p.value
+
+    def stop_test(self):
+        _check(load().rimdp_solve_stop_test(self._h))
 
     def value_buffers(self):
         b0, b1 = C.c_void_p(), C.c_void_p()
