@@ -80,14 +80,16 @@ struct DevBuf {
 
 // Column classes of the scheduler: <= 32 entries ->
 // warp kernel (omax_short); longer columns whose greedy stops after a few
-// picks -> exact warp kernel (omax_long); the rest -> one CTA per column,
-// sorted (omax_sorted), by power-of-two size class 2^6 .. 2^13.
+// picks -> pipelined warp kernel with 2 or 4 entries per lane (omax_medium,
+// <= 64 / <= 128 entries) or the exact warp kernel (omax_long, any length);
+// the rest -> one CTA per column, sorted (omax_sorted), by power-of-two size
+// class 2^6 .. 2^13.
 constexpr int kSortedMinLog = 6, kSortedMaxLog = 13, kSortedClasses = kSortedMaxLog - kSortedMinLog + 1;
 constexpr double kExactPickBudget = 4.0;
 
 struct ColumnLists {
-    DevBuf short_list, exact_list, sorted_list[kSortedClasses];
-    int n_short = 0, n_exact = 0, n_sorted[kSortedClasses] = {};
+    DevBuf short_list, exact_list, medium_list[2], sorted_list[kSortedClasses];
+    int n_short = 0, n_exact = 0, n_medium[2] = {}, n_sorted[kSortedClasses] = {};
     int total_sorted() const {
         int t = 0;
         for (int i = 0; i < kSortedClasses; ++i) t += n_sorted[i];
@@ -145,6 +147,7 @@ struct rimdp_model {
     long long device_bytes = 0;
     int sm_count = 148;
     int short_blocks_per_sm = 4;
+    bool bitonic = false;                     // many-pick long columns: bitonic sort instead of quickselect
     SolveState s;
 };
 
@@ -186,45 +189,60 @@ void upload_list(rimdp_model* m, DevBuf& buf, const std::vector<U>& v) {
     if (!v.empty()) CK(cudaMemcpyAsync(buf.p, v.data(), sizeof(U) * v.size(), cudaMemcpyHostToDevice, m->stream));
 }
 
-// Routing mode for long columns: RIMDP_LONG=exact|sorted forces one path (tests).
+// Routing mode for long columns (tests): RIMDP_LONG=exact (every long column
+// on the exact warp kernel), sorted (every one on the bitonic CTA kernel),
+// select (every one on the quickselect kernels).
 int long_mode() {
     const char* e = getenv("RIMDP_LONG");
     if (!e) return 0;
     if (!strcmp(e, "exact")) return 1;
     if (!strcmp(e, "sorted")) return 2;
+    if (!strcmp(e, "select")) return 3;
     return 0;
 }
 
 // Class of one column given its length, remainder and largest gap.
-//   0: short   1: exact long   2 + i: sorted, size class 2^(kSortedMinLog + i)
+//   0: short   1: exact long   2: medium (E = 2)   3: medium (E = 4)
+//   4 + i: sorted, size class 2^(kSortedMinLog + i)
+constexpr int kClassMedium = 2, kClassSorted = 4;
 int column_class(long long len, double rem, double maxgap, int mode) {
     if (len <= kShortLen) return 0;
     if (len > (1ll << kSortedMaxLog)) return 1; // beyond the largest CTA sort: exact warp kernel
     bool sorted;
     if (mode) {
-        sorted = mode == 2;
+        sorted = mode >= 2;
     } else {
-        // the greedy needs at least rem / maxgap picks; few picks -> exact argmin kernel
+        // the greedy needs at least rem / maxgap picks; few picks -> exact argmin kernels
         sorted = rem > 0 && (maxgap <= 0 || rem > kExactPickBudget * maxgap);
     }
-    if (!sorted) return 1;
+    if (!sorted) {
+        if (mode == 1) return 1;
+        if (len <= 2 * kShortLen) return kClassMedium;
+        if (len <= 4 * kShortLen) return kClassMedium + 1;
+        return 1;
+    }
     int lg = kSortedMinLog;
     while ((1ll << lg) < len) ++lg;
-    return 2 + (lg - kSortedMinLog);
+    return kClassSorted + (lg - kSortedMinLog);
 }
 
 void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, const std::vector<signed char>& cls) {
-    std::vector<int> sh, ex, so[kSortedClasses];
+    std::vector<int> sh, ex, md[2], so[kSortedClasses];
     for (int c : cols) {
         const int k = cls[c];
         if (k == 0) sh.push_back(c);
         else if (k == 1) ex.push_back(c);
-        else so[k - 2].push_back(c);
+        else if (k < kClassSorted) md[k - kClassMedium].push_back(c);
+        else so[k - kClassSorted].push_back(c);
     }
     L.n_short = (int)sh.size();
     L.n_exact = (int)ex.size();
     upload_list(m, L.short_list, sh);
     upload_list(m, L.exact_list, ex);
+    for (int i = 0; i < 2; ++i) {
+        L.n_medium[i] = (int)md[i].size();
+        upload_list(m, L.medium_list[i], md[i]);
+    }
     for (int i = 0; i < kSortedClasses; ++i) {
         L.n_sorted[i] = (int)so[i].size();
         upload_list(m, L.sorted_list[i], so[i]);
@@ -248,6 +266,7 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         CK(cudaStreamSynchronize(m->stream));
     }
     const int mode = long_mode();
+    m->bitonic = mode == 2;
     std::vector<signed char> cls(m->ncols);
     std::vector<int> allc(m->ncols), qc;
     int maxlen = 0;
@@ -319,7 +338,7 @@ void prepare(rimdp_model* m) {
         check_rows<<<grid_for(m->nnz, 256, m->sm_count, 8), 256, 0, m->stream>>>(m->nnz, m->rows.as<int>(), m->n_global,
                                                                               counters + 1);
     if (m->ncols > 0)
-        prepare_columns<T><<<grid_for(m->ncols, 128, m->sm_count, 16), 128, 0, m->stream>>>(
+        prepare_columns<T><<<grid_for(m->ncols, 8, m->sm_count, 8), 256, 0, m->stream>>>(
             m->ncols, m->colptr.as<long long>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(),
             m->infeasible.as<unsigned char>(), m->quoted.as<T>(), m->maxgap.as<T>(), counters);
     CK(cudaGetLastError());
@@ -439,13 +458,55 @@ void launch_sorted_class(rimdp_model* m, int count, const DevBuf& list, const T*
                                                 m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
 }
 
+template <class T, bool P, int LG>
+void launch_select_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
+    using Sh = SelectShape<LG>;
+    auto k = omax_select<T, P, LG>;
+    const size_t smem = Sh::template smem<T>();
+    static bool configured[64] = {};
+    static int per_sm[64] = {};
+    const int dev = m->device & 63;
+    if (!configured[dev]) {
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, Sh::Block, smem));
+        per_sm[dev] = std::max(per_sm[dev], 1);
+        configured[dev] = true;
+    }
+    const int blocks = grid_for(count, Sh::Groups, m->sm_count, per_sm[dev]);
+    k<<<blocks, Sh::Block, smem, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+                                              m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
+}
+
+// Many-pick long columns by size class: weighted quickselect (omax_select,
+// default) or the bitonic-sort kernel (omax_sorted, RIMDP_LONG=sorted).
 template <class T, bool P, int LG = kSortedMinLog>
 void launch_sorted(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl) {
     if constexpr (LG <= kSortedMaxLog) {
         const int i = LG - kSortedMinLog;
-        if (L.n_sorted[i] > 0) launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+        if (L.n_sorted[i] > 0) {
+            if (m->bitonic)
+                launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+            else
+                launch_select_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+        }
         launch_sorted<T, P, LG + 1>(m, L, V, q, ctl);
     }
+}
+
+template <class T, int E>
+void launch_medium(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl, bool pess,
+                   unsigned* work) {
+    using Sh = MediumShape<E>;
+    auto k = pess ? omax_medium<T, true, E> : omax_medium<T, false, E>;
+    static int per_sm[64] = {};
+    const int dev = m->device & 63;
+    if (!per_sm[dev]) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, Sh::W * 32, 0));
+        per_sm[dev] = std::max(per_sm[dev], 1);
+    }
+    const int blocks = grid_for(count, Sh::B * Sh::W, m->sm_count, per_sm[dev]);
+    k<<<blocks, Sh::W * 32, 0, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+                                             m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl, work);
 }
 
 // Per-column expectations q for the columns of one set of class lists.
@@ -458,8 +519,10 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
                                                           m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
                                                           m->rem.as<T>(), V, q, ctl, work);
     }
+    if (L.n_medium[0] > 0) launch_medium<T, 2>(m, L.n_medium[0], L.medium_list[0], V, q, ctl, pess, work + 2);
+    if (L.n_medium[1] > 0) launch_medium<T, 4>(m, L.n_medium[1], L.medium_list[1], V, q, ctl, pess, work + 3);
     if (L.n_exact > 0) {
-        const int blocks = grid_for(L.n_exact, kWarpsPerBlock, m->sm_count, 8);
+        const int blocks = grid_for(L.n_exact, kWarpsPerBlock * kLongGroup, m->sm_count, 8);
         auto k = pess ? omax_long<T, true> : omax_long<T, false>;
         k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(L.n_exact, L.exact_list.as<int>(), m->colptr.as<long long>(),
                                                          m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
@@ -534,7 +597,8 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
 }
 
 int kernels_per_iteration(const rimdp_model* m) {
-    int k = (m->nbatch > 0) + (m->qp.n_short > 0) + (m->qp.n_exact > 0) + (m->nlong_states > 0);
+    int k = (m->nbatch > 0) + (m->qp.n_short > 0) + (m->qp.n_exact > 0) + (m->nlong_states > 0) +
+            (m->qp.n_medium[0] > 0) + (m->qp.n_medium[1] > 0);
     for (int i = 0; i < kSortedClasses; ++i) k += m->qp.n_sorted[i] > 0;
     return k;
 }
@@ -869,7 +933,7 @@ int rimdp_model_info_get(rimdp_model* m, rimdp_model_info* o) {
     o->num_infeasible_columns = (int)m->infeasible_cols.size();
     o->device_bytes = m->device_bytes;
     o->short_columns = m->all.n_short;
-    o->mid_columns = m->all.n_exact;
+    o->mid_columns = m->all.n_exact + m->all.n_medium[0] + m->all.n_medium[1];
     o->long_columns = m->all.total_sorted();
     return RIMDP_OK;
 }

@@ -65,4 +65,36 @@ struct Num<float> {
     }
 };
 
+// ---------------------------------------------------------------------------
+// L2 residency of the value vector.  Per iteration the column kernels stream
+// the transition store once (20 B / transition, far larger than the 126 MB
+// L2) while gathering V[row] at random (n x 8 B).  Streaming loads carry an
+// evict-first policy and the gathers evict-last, so V stays resident in L2
+// instead of being evicted by the stream (config 4: V is 80 MB).
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_hint(const double* a, unsigned long long pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_hint(const float* a, unsigned long long pol) {
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int ld_hint(const int* a, unsigned long long pol) {
+    int v;
+    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
 } // namespace rimdp_dev

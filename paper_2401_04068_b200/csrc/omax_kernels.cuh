@@ -52,38 +52,64 @@ struct Ctl {
 // Model preparation: per-column remainder and feasibility (omax.hpp:64-85),
 // and gap = upper - lower in place of upper.  Sequential in row order, so the
 // sums carry the reference's rounding.
+// One warp per column: coalesced 32-entry chunks; gap = upper - lower and
+// the largest gap are elementwise / order-free, while the two running sums
+// are kept sequential in row order by lanes 0 (lower) and 1 (gap) reading the
+// chunk back from shared memory.
 template <class T>
-__global__ void prepare_columns(int ncols, const long long* __restrict__ colptr, const T* __restrict__ lower,
-                                T* __restrict__ upper_to_gap, T* __restrict__ rem, unsigned char* __restrict__ infeasible,
-                                T* __restrict__ quoted_sum, T* __restrict__ maxgap, int* __restrict__ n_infeasible) {
+__global__ void __launch_bounds__(256)
+prepare_columns(int ncols, const long long* __restrict__ colptr, const T* __restrict__ lower,
+                T* __restrict__ upper_to_gap, T* __restrict__ rem, unsigned char* __restrict__ infeasible,
+                T* __restrict__ quoted_sum, T* __restrict__ maxgap, int* __restrict__ n_infeasible) {
     using N = Num<T>;
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+    __shared__ T st[8][2][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int c = blockIdx.x * 8 + w; c < ncols; c += gridDim.x * 8) {
         const long long b = colptr[c], e = colptr[c + 1];
-        T ls = T(0), gs = T(0), mg = T(0);
-        for (long long i = b; i < e; ++i) {
-            const T g = N::sub(upper_to_gap[i], lower[i]);
-            ls = N::add(ls, lower[i]);
-            gs = N::add(gs, g);
-            mg = g > mg ? g : mg;
-            upper_to_gap[i] = g;
+        T run = T(0), mg = T(0); // lane 0: sum of lower, lane 1: sum of gaps
+        for (long long j0 = b; j0 < e; j0 += 32) {
+            const long long j = j0 + lane;
+            T l = T(0), g = T(0);
+            if (j < e) {
+                l = lower[j];
+                g = N::sub(upper_to_gap[j], l);
+                upper_to_gap[j] = g;
+                mg = g > mg ? g : mg;
+            }
+            st[w][0][lane] = l;
+            st[w][1][lane] = g;
+            __syncwarp();
+            if (lane < 2) {
+                const int m = static_cast<int>(e - j0 < 32 ? e - j0 : 32);
+                for (int i = 0; i < m; ++i) run = N::add(run, st[w][lane][i]);
+            }
+            __syncwarp();
         }
-        maxgap[c] = mg;
-        unsigned char bad = 0;
-        T q = T(0);
-        if (ls > N::add(T(1), N::tol())) {
-            bad = 1;
-            q = ls;
-        } else if (N::add(ls, gs) < N::sub(T(1), N::tol())) {
-            bad = 2;
-            q = N::add(ls, gs);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T x = __shfl_xor_sync(0xffffffffu, mg, o);
+            mg = x > mg ? x : mg;
         }
-        T r = N::sub(T(1), ls);
-        if (r < T(0)) r = T(0);
-        if (r > gs) r = gs;
-        rem[c] = r;
-        infeasible[c] = bad;
-        quoted_sum[c] = q;
-        if (bad) atomicAdd(n_infeasible, 1);
+        const T ls = __shfl_sync(0xffffffffu, run, 0), gs = __shfl_sync(0xffffffffu, run, 1);
+        if (lane == 0) {
+            maxgap[c] = mg;
+            unsigned char bad = 0;
+            T qs = T(0);
+            if (ls > N::add(T(1), N::tol())) {
+                bad = 1;
+                qs = ls;
+            } else if (N::add(ls, gs) < N::sub(T(1), N::tol())) {
+                bad = 2;
+                qs = N::add(ls, gs);
+            }
+            T r = N::sub(T(1), ls);
+            if (r < T(0)) r = T(0);
+            if (r > gs) r = gs;
+            rem[c] = r;
+            infeasible[c] = bad;
+            quoted_sum[c] = qs;
+            if (bad) atomicAdd(n_infeasible, 1);
+        }
     }
 }
 
@@ -308,12 +334,238 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
 }
 
 // ---------------------------------------------------------------------------
-// Long columns (> 32 entries).  One warp per column.  Each greedy step is a
-// warp argmin over the entries strictly after the previous pick in the
-// adversary ordering; only positions whose assignment is clipped by the
-// remaining mass (g >= avail) need their value remembered, every other
-// picked position receives lower + gap.  The expectation is then summed in
-// row order, 32 products at a time, by lane 0.
+// Medium columns (33 .. 32*E entries, few greedy picks): omax_short widened
+// to E entries per lane.  Lane i owns positions i, 32 + i, ..., 32(E-1) + i,
+// so every load is still one coalesced 128/256-byte segment per e.  A warp
+// walks batches of B columns (metadata window: lanes [0, B) the current
+// batch, [B, 2B) the next), with the same three-deep pipeline: the rows of
+// column i+2 and (lower, gap, V[row]) of column i+1 are in flight while
+// column i is reduced.  Each greedy pick is an exact warp argmin of
+// (key, position): every lane first takes the minimum of its own E entries
+// (its positions increase with e, so the first minimum wins ties), then the
+// warp reduces the key words and the position.  Products are staged in
+// shared memory and lane t < B sums column t in row order, so the result is
+// bit-identical to the reference (omax.hpp:98-112, 169-173).
+template <int E>
+struct MediumShape {
+    static constexpr int B = E == 2 ? 8 : 4;       // columns per batch
+    static constexpr int W = 8;                    // warps per block
+    static constexpr int Len = 32 * E;
+};
+
+template <class T, bool kPess, int E>
+__global__ void __launch_bounds__(MediumShape<E>::W * 32)
+omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+            const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+            const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl,
+            unsigned* __restrict__ work) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    using Sh = MediumShape<E>;
+    constexpr int B = Sh::B, W = Sh::W, LEN = Sh::Len;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    __shared__ T xs[W][B][LEN + 1];
+    const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * W + w, nw = gridDim.x * W;
+    auto next_batch = [&]() -> int {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(work, 1u);
+        return nw + static_cast<int>(__shfl_sync(kFull, t, 0));
+    };
+    int base = gw * B;
+    if (base >= nlist) return;
+    int nbase = next_batch() * B;
+
+    int mc = -1, mlen = 0;
+    long long mbeg = 0;
+    T mrem = T(0);
+    auto load_meta = [&](int batch_base) {
+        const int idx = batch_base + (lane & (B - 1));
+        mc = -1;
+        mlen = 0;
+        mbeg = 0;
+        mrem = T(0);
+        if (lane < 2 * B && idx < nlist) {
+            mc = __ldg(list + idx);
+            mbeg = __ldg(colptr + mc);
+            mlen = static_cast<int>(__ldg(colptr + mc + 1) - mbeg);
+            mrem = __ldg(rem + mc);
+        }
+    };
+    load_meta(lane < B ? base : nbase);
+
+    long long bn = __shfl_sync(kFull, mbeg, 0), bnn = __shfl_sync(kFull, mbeg, 1);
+    int Ln = __shfl_sync(kFull, mlen, 0), Lnn = __shfl_sync(kFull, mlen, 1);
+    int rowA[E], rowB[E];
+    T lc[E], gc[E], vc[E], ln[E], gn[E], vn[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int j = e * 32 + lane;
+        rowA[e] = j < Ln ? ld_hint(rows + bn + j, pstream) : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int j = e * 32 + lane;
+        lc[e] = gc[e] = vc[e] = T(0);
+        if (j < Ln) {
+            lc[e] = ld_hint(lower + bn + j, pstream);
+            gc[e] = ld_hint(gap + bn + j, pstream);
+            vc[e] = ld_hint(V + rowA[e], pval);
+        }
+    }
+    int Lc = Ln;
+    bn = bnn;
+    Ln = Lnn;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int j = e * 32 + lane;
+        rowA[e] = j < Ln ? ld_hint(rows + bn + j, pstream) : 0;
+    }
+    bnn = __shfl_sync(kFull, mbeg, 2);
+    Lnn = __shfl_sync(kFull, mlen, 2);
+
+    for (;;) {
+        for (int s = 0; s < B; ++s) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int j = e * 32 + lane;
+                ln[e] = gn[e] = vn[e] = T(0);
+                if (j < Ln) {
+                    ln[e] = ld_hint(lower + bn + j, pstream);
+                    gn[e] = ld_hint(gap + bn + j, pstream);
+                    vn[e] = ld_hint(V + rowA[e], pval);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int j = e * 32 + lane;
+                rowB[e] = j < Lnn ? ld_hint(rows + bnn + j, pstream) : 0;
+            }
+            // greedy O-max of column s (omax.hpp:98-112)
+            const T r = __shfl_sync(kFull, mrem, s);
+            Bits key[E];
+            T p[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                key[e] = e * 32 + lane < Lc ? order_key<T>(vc[e], kPess) : ~Bits(0);
+                p[e] = lc[e];
+            }
+            T consumed = T(0), avail = r;
+            for (int nsel = 0; avail > T(0) && nsel < Lc; ++nsel) {
+                // lane-local (key, e) minimum, then the warp-wide one
+                Bits bk = key[0];
+                int be = 0;
+#pragma unroll
+                for (int e = 1; e < E; ++e)
+                    if (key[e] < bk) {
+                        bk = key[e];
+                        be = e;
+                    }
+                bool cand = true;
+                if constexpr (sizeof(Bits) == 8) {
+                    const unsigned hi = static_cast<unsigned>(bk >> 32), lo = static_cast<unsigned>(bk);
+                    const unsigned mhi = __reduce_min_sync(kFull, hi);
+                    cand = hi == mhi;
+                    const unsigned mlo = __reduce_min_sync(kFull, cand ? lo : 0xffffffffu);
+                    cand = cand && lo == mlo;
+                } else {
+                    const unsigned mk = __reduce_min_sync(kFull, static_cast<unsigned>(bk));
+                    cand = static_cast<unsigned>(bk) == mk;
+                }
+                const unsigned pos = __reduce_min_sync(kFull, cand ? static_cast<unsigned>(be * 32 + lane) : 0xffffffffu);
+                const int sel_lane = static_cast<int>(pos & 31u), sel_e = static_cast<int>(pos >> 5);
+                T mine = gc[0];
+#pragma unroll
+                for (int e = 1; e < E; ++e)
+                    if (e == sel_e) mine = gc[e];
+                const T gs = __shfl_sync(kFull, mine, sel_lane);
+                if (lane == sel_lane) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e)
+                        if (e == sel_e) {
+                            p[e] = N::add(lc[e], gc[e] < avail ? gc[e] : avail);
+                            key[e] = ~Bits(0);
+                        }
+                }
+                consumed = N::add(consumed, gs);
+                avail = N::sub(r, consumed);
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                if (e * 32 + lane < Lc) xs[w][s][e * 32 + lane] = N::mul(vc[e], p[e]);
+            // rotate the pipeline
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                lc[e] = ln[e];
+                gc[e] = gn[e];
+                vc[e] = vn[e];
+                rowA[e] = rowB[e];
+            }
+            Lc = Ln;
+            bn = bnn;
+            Ln = Lnn;
+            bnn = __shfl_sync(kFull, mbeg, s + 3);
+            Lnn = __shfl_sync(kFull, mlen, s + 3);
+        }
+        __syncwarp();
+        if (lane < B && mc >= 0) {
+            T acc = T(0);
+            for (int i = 0; i < mlen; ++i) acc = N::add(acc, xs[w][lane][i]);
+            q[mc] = acc;
+        }
+        __syncwarp();
+        base = nbase;
+        if (base >= nlist) break;
+        nbase = next_batch() * B;
+        const int c2 = __shfl_down_sync(kFull, mc, B);
+        const long long b2 = __shfl_down_sync(kFull, mbeg, B);
+        const int l2 = __shfl_down_sync(kFull, mlen, B);
+        const T r2 = __shfl_down_sync(kFull, mrem, B);
+        if (lane < B) {
+            mc = c2;
+            mbeg = b2;
+            mlen = l2;
+            mrem = r2;
+        } else {
+            load_meta(nbase);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Long columns (> 32 entries) with few greedy picks.  One warp per group of
+// kLongGroup columns.
+//
+// Phase A, one column at a time — scan: one coalesced pass over the column
+// (rows, V[row]; four 32-entry chunks in flight per lane) in which every
+// lane keeps its kLongTopK smallest (order key, position, gap) in a register
+// list.  Greedy: each pick is an exact warp argmin over the lanes' list
+// heads; the winner pops its head.  The lists hold every position the greedy
+// can reach before some lane runs dry — if one does while it still owns
+// unseen positions, the greedy continues with full rescans: a warp argmin
+// over the entries strictly after the previous pick.  Only positions whose
+// assignment is clipped by the remaining mass (g >= avail) need their value
+// remembered; every other picked position receives lower + gap.  The result
+// (last pick, clipped positions) goes to shared memory.
+//
+// Phase B, the group's columns interleaved: chunk by chunk (32 entries of
+// each column), the warp forms the products V[row] * p in shared memory and
+// lane j adds column j's 32 products to its running sum — sequentially in
+// row order, so bit-exact (omax.hpp:169-173), with the group's sums advancing
+// in parallel instead of one lane summing one column.
+constexpr int kLongTopK = 4;
+constexpr int kLongGroup = 8;
+
+template <class T>
+struct LongCut {
+    typename Num<T>::Bits lastk;
+    int lastp;   // -1: nothing picked
+    int npart;
+    int ppos[kMaxPartial];
+    T pval[kMaxPartial];
+};
+
 template <class T, bool kPess>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
@@ -321,83 +573,214 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
           const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, Ctl* __restrict__ ctl) {
     using N = Num<T>;
     using Bits = typename N::Bits;
+    constexpr int K = kLongTopK, U = 4, G = kLongGroup;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
-    __shared__ T xs[kWarpsPerBlock][32];
+    __shared__ T xs[kWarpsPerBlock][G][33];
+    __shared__ LongCut<T> cuts[kWarpsPerBlock][G];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
-    for (int i = gw; i < nlist; i += nw) {
-        const int c = list[i];
-        const long long b = colptr[c];
-        const int L = static_cast<int>(colptr[c + 1] - b);
-        const T r = rem[c];
-        // greedy along the adversary ordering
-        bool any = false;
-        Bits lastk = 0;
-        int lastp = -1;
-        int npart = 0;
-        int ppos[kMaxPartial];
-        T pval[kMaxPartial];
-        T consumed = T(0);
-        for (;;) {
-            const T avail = N::sub(r, consumed);
-            if (!(avail > T(0))) break;
-            Bits bk = ~Bits(0);
-            int bp = INT_MAX;
-            bool have = false;
-            for (int j = lane; j < L; j += 32) {
-                const Bits k = N::key(__ldg(V + __ldg(rows + b + j)), kPess);
-                const bool after = !any || k > lastk || (k == lastk && j > lastp);
-                if (after && (!have || k < bk || (k == bk && j < bp))) {
-                    bk = k;
-                    bp = j;
-                    have = true;
-                }
-            }
-            Bits mk;
-            int mp;
-            if (!warp_argmin_pos(bk, bp, have, mk, mp)) break;
-            const T g = __ldg(gap + b + mp);
-            if (!(g < avail)) {
-                if (npart < kMaxPartial) {
-                    ppos[npart] = mp;
-                    pval[npart] = N::add(__ldg(lower + b + mp), avail);
-                }
-                ++npart;
-            }
-            consumed = N::add(consumed, g);
-            any = true;
-            lastk = mk;
-            lastp = mp;
+    for (int base = gw * G; base < nlist; base += nw * G) {
+        // lane j < G describes column j of the group
+        int mc = -1, mlen = 0;
+        long long mbeg = 0;
+        T mrem = T(0);
+        if (lane < G && base + lane < nlist) {
+            mc = __ldg(list + base + lane);
+            mbeg = __ldg(colptr + mc);
+            mlen = static_cast<int>(__ldg(colptr + mc + 1) - mbeg);
+            mrem = __ldg(rem + mc);
         }
-        if (npart > kMaxPartial && lane == 0 && ctl) atomicExch(&ctl->status, 2);
-        // expectation in row order
-        T acc = T(0);
-        for (int j0 = 0; j0 < L; j0 += 32) {
-            const int j = j0 + lane;
-            T x = T(0);
-            if (j < L) {
-                const T v = __ldg(V + __ldg(rows + b + j));
-                const T l = __ldg(lower + b + j);
-                T p = l;
-                if (any) {
-                    const Bits k = N::key(v, kPess);
-                    if (k < lastk || (k == lastk && j <= lastp)) {
-                        p = N::add(l, __ldg(gap + b + j));
-                        for (int t = 0; t < npart && t < kMaxPartial; ++t)
-                            if (ppos[t] == j) p = pval[t];
+        const int ng = min(G, nlist - base);
+        // ---- phase A: greedy of each column ----
+        for (int jc = 0; jc < ng; ++jc) {
+            const long long b = __shfl_sync(kFull, mbeg, jc);
+            const int L = __shfl_sync(kFull, mlen, jc);
+            const T r = __shfl_sync(kFull, mrem, jc);
+            Bits hk[K];
+            int hp[K];
+            T hg[K];
+#pragma unroll
+            for (int t = 0; t < K; ++t) {
+                hk[t] = ~Bits(0);
+                hp[t] = INT_MAX;
+                hg[t] = T(0);
+            }
+            int seen = 0;
+            for (int j0 = 0; j0 < L; j0 += 32 * U) {
+                int rw[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + u * 32 + lane;
+                    rw[u] = j < L ? __ldg(rows + b + j) : 0;
+                }
+                T vv[U], gg[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + u * 32 + lane;
+                    vv[u] = j < L ? __ldg(V + rw[u]) : T(0);
+                    gg[u] = j < L ? __ldg(gap + b + j) : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + u * 32 + lane;
+                    if (j < L) {
+                        ++seen;
+                        const Bits k = N::key(vv[u], kPess);
+                        // positions of a lane increase, so an equal key ranks after: strict <
+                        if (k < hk[K - 1]) {
+                            Bits ck = k;
+                            int cp = j;
+                            T cg = gg[u];
+#pragma unroll
+                            for (int t = 0; t < K; ++t) {
+                                // a displaced entry can tie the next one: order by (key, pos)
+                                if (ck < hk[t] || (ck == hk[t] && cp < hp[t])) {
+                                    const Bits tk = hk[t];
+                                    const int tp = hp[t];
+                                    const T tg = hg[t];
+                                    hk[t] = ck;
+                                    hp[t] = cp;
+                                    hg[t] = cg;
+                                    ck = tk;
+                                    cp = tp;
+                                    cg = tg;
+                                }
+                            }
+                        }
                     }
                 }
-                x = N::mul(v, p);
             }
-            xs[w][lane] = x;
-            __syncwarp();
+            // greedy along the adversary ordering (omax.hpp:98-112)
+            bool any = false;
+            Bits lastk = 0;
+            int lastp = -1;
+            int npart = 0;
+            int ppos[kMaxPartial];
+            T pval[kMaxPartial];
+            T consumed = T(0);
+            int popped = 0;
+            bool dry = false; // some lane emptied its list while owning unseen positions
+            for (;;) {
+                const T avail = N::sub(r, consumed);
+                if (!(avail > T(0))) break;
+                if (__any_sync(kFull, dry)) break;
+                Bits mk;
+                int mp;
+                if (!warp_argmin_pos(hk[0], hp[0], hp[0] != INT_MAX, mk, mp)) break; // every position picked
+                const bool mine = hp[0] == mp;
+                const T g = __shfl_sync(kFull, hg[0], __ffs(__ballot_sync(kFull, mine)) - 1);
+                if (mine) {
+#pragma unroll
+                    for (int t = 0; t < K - 1; ++t) {
+                        hk[t] = hk[t + 1];
+                        hp[t] = hp[t + 1];
+                        hg[t] = hg[t + 1];
+                    }
+                    hk[K - 1] = ~Bits(0);
+                    hp[K - 1] = INT_MAX;
+                    ++popped;
+                    dry = hp[0] == INT_MAX && seen > popped;
+                }
+                if (!(g < avail)) {
+                    if (npart < kMaxPartial) {
+                        ppos[npart] = mp;
+                        pval[npart] = N::add(__ldg(lower + b + mp), avail);
+                    }
+                    ++npart;
+                }
+                consumed = N::add(consumed, g);
+                any = true;
+                lastk = mk;
+                lastp = mp;
+            }
+            // continuation with full rescans once a lane's list ran dry
+            if (__any_sync(kFull, dry)) {
+                for (;;) {
+                    const T avail = N::sub(r, consumed);
+                    if (!(avail > T(0))) break;
+                    Bits bk = ~Bits(0);
+                    int bp = INT_MAX;
+                    bool have = false;
+                    for (int j = lane; j < L; j += 32) {
+                        const Bits k = N::key(__ldg(V + __ldg(rows + b + j)), kPess);
+                        const bool after = !any || k > lastk || (k == lastk && j > lastp);
+                        if (after && (!have || k < bk || (k == bk && j < bp))) {
+                            bk = k;
+                            bp = j;
+                            have = true;
+                        }
+                    }
+                    Bits mk;
+                    int mp;
+                    if (!warp_argmin_pos(bk, bp, have, mk, mp)) break;
+                    const T g = __ldg(gap + b + mp);
+                    if (!(g < avail)) {
+                        if (npart < kMaxPartial) {
+                            ppos[npart] = mp;
+                            pval[npart] = N::add(__ldg(lower + b + mp), avail);
+                        }
+                        ++npart;
+                    }
+                    consumed = N::add(consumed, g);
+                    any = true;
+                    lastk = mk;
+                    lastp = mp;
+                }
+            }
+            if (npart > kMaxPartial && lane == 0 && ctl) atomicExch(&ctl->status, 2);
             if (lane == 0) {
-                const int m = min(32, L - j0);
-                for (int t = 0; t < m; ++t) acc = N::add(acc, xs[w][t]);
+                LongCut<T>& cu = cuts[w][jc];
+                cu.lastk = lastk;
+                cu.lastp = any ? lastp : -1;
+                cu.npart = npart < kMaxPartial ? npart : kMaxPartial;
+                for (int t = 0; t < kMaxPartial; ++t) {
+                    cu.ppos[t] = t < npart ? ppos[t] : -1;
+                    cu.pval[t] = t < npart ? pval[t] : T(0);
+                }
+            }
+        }
+        __syncwarp();
+        // ---- phase B: row-order expectations of the group, chunk by chunk ----
+        const int maxL = __reduce_max_sync(kFull, static_cast<unsigned>(mlen));
+        T acc = T(0);
+        for (int j0 = 0; j0 < maxL; j0 += 32) {
+            const int j = j0 + lane;
+            int rw[G];
+#pragma unroll
+            for (int jc = 0; jc < G; ++jc) {
+                const long long b = __shfl_sync(kFull, mbeg, jc);
+                const int L = __shfl_sync(kFull, mlen, jc);
+                rw[jc] = (jc < ng && j < L) ? __ldg(rows + b + j) : 0;
+            }
+#pragma unroll
+            for (int jc = 0; jc < G; ++jc) {
+                const long long b = __shfl_sync(kFull, mbeg, jc);
+                const int L = __shfl_sync(kFull, mlen, jc);
+                if (jc < ng && j < L) {
+                    const T v = __ldg(V + rw[jc]);
+                    const T l = __ldg(lower + b + j);
+                    const LongCut<T>& cu = cuts[w][jc];
+                    T p = l;
+                    if (cu.lastp >= 0) {
+                        const Bits k = N::key(v, kPess);
+                        if (k < cu.lastk || (k == cu.lastk && j <= cu.lastp)) {
+                            p = N::add(l, __ldg(gap + b + j));
+                            for (int t = 0; t < cu.npart; ++t)
+                                if (cu.ppos[t] == j) p = cu.pval[t];
+                        }
+                    }
+                    xs[w][jc][lane] = N::mul(v, p);
+                }
+            }
+            __syncwarp();
+            if (lane < ng) {
+                const int m = min(32, mlen - j0);
+                for (int t = 0; t < m; ++t) acc = N::add(acc, xs[w][lane][t]);
             }
             __syncwarp();
         }
-        if (lane == 0) q[c] = acc;
+        if (lane < ng) q[mc] = acc;
+        __syncwarp();
     }
 }
 
@@ -579,6 +962,238 @@ omax_sorted(int nlist, const int* __restrict__ list, const long long* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// Long columns with many greedy picks (33 .. 8192 entries): weighted
+// quickselect of the greedy's cut instead of a full sort.
+//
+// The greedy (omax.hpp:98-112) gives every position before the cut c its
+// full gap, c the rest of the remainder and every later position nothing,
+// where c is the last position (in the adversary order) whose prefix gap
+// sum F(c) = sum of the gaps ordered before it is < rem.  So only c and
+// F(c) are needed, not the order itself.  They are found by quickselect on
+// the composite key (order key of V[row], position): each pass splits the
+// candidate set at a pivot element into Left (< pivot) and Right (>= pivot),
+// one group-wide reduction yields the Left gap sum; if base + sum(Left) <
+// rem the cut is in Right (base += sum(Left)), otherwise in Left.  The next
+// pivot is the candidate of the chosen side with the smallest pseudo-random
+// priority h(pos) = pos * 0x9E3779B1 mod 2^13 (a bijection, so the position
+// is recovered from the reduced minimum).  Expected passes ~ 2 ln L (a
+// random BST's depth): ~8 at L = 64, ~17 at L = 4096, against log2(L)^2 / 2
+// barrier stages for a bitonic sort.
+//
+// Work unit: one warp per column (NT = 32: no barriers) up to 512 entries,
+// one CTA per column (NT = 256 / 512: one barrier per pass, partials double
+// buffered) beyond.  Thread t of the group owns positions e * NT + t, so
+// every load is coalesced.  Gap sums are in tree order, so, like
+// omax_sorted, results are within a few ulps of the reference (tests bound
+// them by 1e-12 per step); deterministic.
+template <int LG>
+struct SelectShape {
+    // LG = ceil(log2(max entries)): 6..9 warp per column, 10..13 CTA per column
+    static constexpr int NT = LG <= 9 ? 32 : (LG <= 12 ? 256 : 512);
+    static constexpr int E = (1 << LG) / NT;
+    static constexpr int Block = NT == 32 ? 256 : NT;
+    static constexpr int Groups = Block / NT;
+    template <class T>
+    static constexpr size_t smem() {
+        // keys (8 B per entry, either dtype) + CTA partials: 2 x NW sums, 8 x NW words
+        return Groups * (1 << LG) * 8 + (NT == 32 ? 0 : (NT / 32) * (2 * sizeof(T) + 32));
+    }
+};
+
+constexpr unsigned kSelMul = 0x9E3779B1u, kSelInv = 0x0E8B2F51u; // kSelMul * kSelInv == 1 mod 2^32
+constexpr unsigned kSelMask = (1u << 13) - 1;
+__device__ __forceinline__ unsigned sel_hash(unsigned pos) { return (pos * kSelMul) & kSelMask; }
+__device__ __forceinline__ unsigned sel_unhash(unsigned h) { return (h * kSelInv) & kSelMask; }
+
+template <class T>
+__device__ __forceinline__ T value_of_key(typename Num<T>::Bits k, bool pess) {
+    using Bits = typename Num<T>::Bits;
+    constexpr Bits kMsb = Bits(1) << (8 * sizeof(Bits) - 1);
+    const Bits b = pess ? k : ~k;
+    const Bits raw = (b & kMsb) ? (b & ~kMsb) : ~b;
+    T v;
+    memcpy(&v, &raw, sizeof v);
+    return v;
+}
+
+template <class T, bool kPess, int LG>
+__global__ void __launch_bounds__(SelectShape<LG>::Block)
+omax_select(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+            const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+            const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    using Sh = SelectShape<LG>;
+    constexpr int NT = Sh::NT, E = Sh::E, NW = NT / 32;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int grp = threadIdx.x / NT, t = threadIdx.x % NT, wig = t >> 5;
+    Bits* skey = reinterpret_cast<Bits*>(smem_raw) + grp * (1 << LG);
+    // CTA groups: per-warp partials, double buffered by pass parity
+    T* ps = reinterpret_cast<T*>(smem_raw + Sh::Groups * (1 << LG) * 8);
+    unsigned* pu = reinterpret_cast<unsigned*>(ps + 2 * NW); // [0, NW): first pivot; [2 NW, 8 NW): passes
+    const int ngroups = gridDim.x * Sh::Groups;
+
+    for (int item = blockIdx.x * Sh::Groups + grp; item < nlist; item += ngroups) {
+        const int c = __ldg(list + item);
+        const long long b = __ldg(colptr + c);
+        const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
+        const T r = __ldg(rem + c);
+        int rw[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = e * NT + t;
+            rw[e] = pos < L ? __ldg(rows + b + pos) : 0;
+        }
+        Bits key[E];
+        T g[E];
+        unsigned cand = 0;
+        unsigned hmin = 0xffffffffu;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = e * NT + t;
+            key[e] = ~Bits(0);
+            g[e] = T(0);
+            if (pos < L) {
+                key[e] = order_key<T>(__ldg(V + rw[e]), kPess);
+                g[e] = __ldg(gap + b + pos);
+                cand |= 1u << e;
+                const unsigned h = sel_hash(static_cast<unsigned>(pos));
+                hmin = h < hmin ? h : hmin;
+            }
+            skey[pos] = key[e];
+        }
+        // first pivot: the valid position with the smallest priority
+        hmin = __reduce_min_sync(kFull, hmin);
+        if constexpr (NW > 1) {
+            if (lane == 0) pu[wig] = hmin;
+            __syncthreads();
+            hmin = pu[0];
+#pragma unroll
+            for (int i = 1; i < NW; ++i) hmin = pu[i] < hmin ? pu[i] : hmin;
+            __syncthreads();
+        } else {
+            __syncwarp();
+        }
+        int pp = static_cast<int>(sel_unhash(hmin));
+        Bits pk = skey[pp];
+        T base = T(0);
+        int ncand = L;
+        int cpos = -1; // the cut position (none when rem <= 0)
+        Bits ckey = 0;
+        if (r > T(0)) {
+            for (int pass = 0;; ++pass) {
+                T sl = T(0);
+                int nl = 0;
+                unsigned hl = 0xffffffffu, hr = 0xffffffffu, lm = 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if (cand >> e & 1u) {
+                        const int pos = e * NT + t;
+                        const bool lt = key[e] < pk || (key[e] == pk && pos < pp);
+                        const unsigned h = sel_hash(static_cast<unsigned>(pos));
+                        if (lt) {
+                            sl = N::add(sl, g[e]);
+                            ++nl;
+                            lm |= 1u << e;
+                            hl = h < hl ? h : hl;
+                        } else if (pos != pp) {
+                            hr = h < hr ? h : hr;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sl = N::add(sl, __shfl_xor_sync(kFull, sl, o));
+                nl = static_cast<int>(__reduce_add_sync(kFull, static_cast<unsigned>(nl)));
+                hl = __reduce_min_sync(kFull, hl);
+                hr = __reduce_min_sync(kFull, hr);
+                if constexpr (NW > 1) {
+                    const int buf = pass & 1;
+                    if (lane == 0) {
+                        ps[buf * NW + wig] = sl;
+                        pu[2 * NW + (buf * NW + wig) * 3 + 0] = static_cast<unsigned>(nl);
+                        pu[2 * NW + (buf * NW + wig) * 3 + 1] = hl;
+                        pu[2 * NW + (buf * NW + wig) * 3 + 2] = hr;
+                    }
+                    __syncthreads();
+                    sl = ps[buf * NW];
+                    nl = static_cast<int>(pu[2 * NW + buf * NW * 3]);
+                    hl = pu[2 * NW + buf * NW * 3 + 1];
+                    hr = pu[2 * NW + buf * NW * 3 + 2];
+#pragma unroll
+                    for (int i = 1; i < NW; ++i) {
+                        sl = N::add(sl, ps[buf * NW + i]);
+                        nl += static_cast<int>(pu[2 * NW + (buf * NW + i) * 3]);
+                        const unsigned a = pu[2 * NW + (buf * NW + i) * 3 + 1];
+                        const unsigned z = pu[2 * NW + (buf * NW + i) * 3 + 2];
+                        hl = a < hl ? a : hl;
+                        hr = z < hr ? z : hr;
+                    }
+                }
+                if (N::add(base, sl) < r) { // the cut is in Right (>= pivot)
+                    base = N::add(base, sl);
+                    cand &= ~lm;
+                    ncand -= nl;
+                    if (ncand == 1) {
+                        cpos = pp;
+                        ckey = pk;
+                        break;
+                    }
+                    pp = static_cast<int>(sel_unhash(hr));
+                } else { // the cut is in Left
+                    cand &= lm;
+                    ncand = nl;
+                    if (ncand == 1) {
+                        cpos = static_cast<int>(sel_unhash(hl));
+                        ckey = skey[cpos];
+                        break;
+                    }
+                    pp = static_cast<int>(sel_unhash(hl));
+                }
+                pk = skey[pp];
+            }
+        }
+        // expectation: positions before the cut take lower + gap, the cut
+        // lower + min(gap, rem - F(cut)), the rest lower (tree order sum)
+        const T availc = N::sub(r, base);
+        T acc = T(0);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = e * NT + t;
+            if (pos < L) {
+                const T l = __ldg(lower + b + pos);
+                T p = l;
+                if (cpos >= 0) {
+                    if (pos == cpos)
+                        p = N::add(l, g[e] < availc ? g[e] : availc);
+                    else if (key[e] < ckey || (key[e] == ckey && pos < cpos))
+                        p = N::add(l, g[e]);
+                }
+                acc = N::add(acc, N::mul(value_of_key<T>(key[e], kPess), p));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = N::add(acc, __shfl_xor_sync(kFull, acc, o));
+        if constexpr (NW > 1) {
+            // partial slots of pass parity 0/1 are free again only after a barrier
+            __syncthreads();
+            if (lane == 0) ps[wig] = acc;
+            __syncthreads();
+            if (t == 0) {
+                T s = ps[0];
+                for (int i = 1; i < NW; ++i) s = N::add(s, ps[i]);
+                q[c] = s;
+            }
+            __syncthreads();
+        } else {
+            if (lane == 0) q[c] = acc;
+            __syncwarp();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Action reduction + reach/avoid/discount update + residual + stop test
 // (bellman.hpp:88-115, solver.hpp:107-134).  Each block folds its max of
 // |V_k - V_{k-1}| into ctl with one atomicMax; the launch flagged `finalize`
@@ -604,7 +1219,7 @@ struct ActionArgs {
     unsigned* work;                // work counters [2 slots][kWorkKinds], slot k & 1
 };
 
-constexpr int kWorkKinds = 4;      // 0: omax_short (q path), 1: bellman_short, 2: omax_long
+constexpr int kWorkKinds = 4;      // 0: omax_short (q path), 1: bellman_short, 2/3: omax_medium E = 2/4
 
 __device__ __forceinline__ const int* forced_row(const ActionArgs& a) {
     return a.forced ? a.forced + (a.forced_td ? (a.horizon - a.k) * (long long)a.n : 0) : nullptr;

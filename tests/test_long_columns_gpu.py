@@ -68,16 +68,37 @@ def test_scheduler_routes_power_law_columns_to_the_sorted_path(powerlaw):
     assert info.short_columns + info.mid_columns + info.long_columns == m.num_cols
 
 
+@pytest.mark.parametrize("mode", ["default", "select", "sorted"])
 @pytest.mark.parametrize("pess", [True, False])
-def test_sorted_columns_within_tolerance(powerlaw, pess):
+def test_sorted_columns_within_tolerance(powerlaw, pess, mode):
+    """default: many-pick columns on the quickselect kernels; select: every
+    long column there (few-pick ones too); sorted: every long column on the
+    bitonic-sort kernel."""
     v = tricky_values(9000, 3)
     ref = ref_columns(powerlaw, v, pess)
-    q = engine.DeviceModel.from_csc(*powerlaw).column_values(v, pess)
+    make = (lambda: engine.DeviceModel.from_csc(*powerlaw))
+    m = make() if mode == "default" else with_long_mode(mode, make)
+    q = m.column_values(v, pess)
     err = np.abs(q - ref)
-    assert err.max() <= COL_TOL, (err.max(), int(err.argmax()))
+    assert err.max() <= COL_TOL, (err.max(), int(err.argmax()), int(np.diff(powerlaw[1])[err.argmax()]))
     # deterministic: a second model gives the same bits
-    q2 = engine.DeviceModel.from_csc(*powerlaw).column_values(v, pess)
-    assert np.array_equal(bits(q), bits(q2))
+    m2 = make() if mode == "default" else with_long_mode(mode, make)
+    assert np.array_equal(bits(q), bits(m2.column_values(v, pess)))
+
+
+@pytest.mark.parametrize("pess", [True, False])
+def test_select_random_values_within_tolerance(powerlaw, pess):
+    """Continuous values (no ties) and the f32 store of the same columns."""
+    v = np.random.default_rng(8).random(9000)
+    ref = ref_columns(powerlaw, v, pess)
+    q = with_long_mode("select", lambda: engine.DeviceModel.from_csc(*powerlaw)).column_values(v, pess)
+    assert np.abs(q - ref).max() <= COL_TOL
+    sp, cp, rv, lo, up = powerlaw
+    arr32 = (sp, cp, rv, lo.astype(np.float32), up.astype(np.float32))
+    v32 = v.astype(np.float32)
+    ref32 = ref_columns(arr32, v32, pess)
+    q32 = with_long_mode("select", lambda: engine.DeviceModel.from_csc(*arr32)).column_values(v32, pess)
+    assert np.abs(q32.astype(np.float64) - ref32).max() <= 1e-5
 
 
 @pytest.mark.parametrize("pess", [True, False])
