@@ -88,8 +88,8 @@ constexpr int kSortedMinLog = 6, kSortedMaxLog = 13, kSortedClasses = kSortedMax
 constexpr double kExactPickBudget = 4.0;
 
 struct ColumnLists {
-    DevBuf short_list, exact_list, medium_list[2], sorted_list[kSortedClasses];
-    int n_short = 0, n_exact = 0, n_medium[2] = {}, n_sorted[kSortedClasses] = {};
+    DevBuf short_list, exact_list, medium_list[2], tiny_list[3], sorted_list[kSortedClasses];
+    int n_short = 0, n_exact = 0, n_medium[2] = {}, n_tiny[3] = {}, n_sorted[kSortedClasses] = {};
     int total_sorted() const {
         int t = 0;
         for (int i = 0; i < kSortedClasses; ++i) t += n_sorted[i];
@@ -148,6 +148,7 @@ struct rimdp_model {
     int sm_count = 148;
     int short_blocks_per_sm = 4;
     bool bitonic = false;                     // many-pick long columns: bitonic sort instead of quickselect
+    size_t l2_persist = 0;                    // bytes of L2 set aside for the value vector (0: none)
     SolveState s;
 };
 
@@ -204,8 +205,12 @@ int long_mode() {
 // Class of one column given its length, remainder and largest gap.
 //   0: short   1: exact long   2: medium (E = 2)   3: medium (E = 4)
 //   4 + i: sorted, size class 2^(kSortedMinLog + i)
-constexpr int kClassMedium = 2, kClassSorted = 4;
+//   kClassTiny + i: <= 4 << i entries (i = 0, 1, 2), several columns per warp
+constexpr int kClassMedium = 2, kClassSorted = 4, kClassTiny = 16;
 int column_class(long long len, double rem, double maxgap, int mode) {
+    if (len <= 4) return kClassTiny;
+    if (len <= 8) return kClassTiny + 1;
+    if (len <= 16) return kClassTiny + 2;
     if (len <= kShortLen) return 0;
     if (len > (1ll << kSortedMaxLog)) return 1; // beyond the largest CTA sort: exact warp kernel
     bool sorted;
@@ -227,10 +232,11 @@ int column_class(long long len, double rem, double maxgap, int mode) {
 }
 
 void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, const std::vector<signed char>& cls) {
-    std::vector<int> sh, ex, md[2], so[kSortedClasses];
+    std::vector<int> sh, ex, md[2], ti[3], so[kSortedClasses];
     for (int c : cols) {
         const int k = cls[c];
         if (k == 0) sh.push_back(c);
+        else if (k >= kClassTiny) ti[k - kClassTiny].push_back(c);
         else if (k == 1) ex.push_back(c);
         else if (k < kClassSorted) md[k - kClassMedium].push_back(c);
         else so[k - kClassSorted].push_back(c);
@@ -242,6 +248,10 @@ void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, co
     for (int i = 0; i < 2; ++i) {
         L.n_medium[i] = (int)md[i].size();
         upload_list(m, L.medium_list[i], md[i]);
+    }
+    for (int i = 0; i < 3; ++i) {
+        L.n_tiny[i] = (int)ti[i].size();
+        upload_list(m, L.tiny_list[i], ti[i]);
     }
     for (int i = 0; i < kSortedClasses; ++i) {
         L.n_sorted[i] = (int)so[i].size();
@@ -284,7 +294,7 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         const int na = sp[s + 1] - sp[s];
         if (na < 1 || na > kShortBatch) return false;
         for (int c = sp[s]; c < sp[s + 1]; ++c)
-            if (cls[c] != 0) return false;
+            if (cls[c] != 0 && cls[c] < kClassTiny) return false;
         return true;
     };
     std::vector<int> slots, lstates;
@@ -377,6 +387,39 @@ void init_common(rimdp_model* m, int device) {
     if (const char* e = getenv("RIMDP_SHORT_BLOCKS")) m->short_blocks_per_sm = atoi(e) == 5 ? 5 : 4;
 }
 
+// L2 residency of the gathered value vector: when
+// V is large (config 4: 80 MB) the stream of column data evicts it from L2
+// and every V[row] gather costs a 32-byte DRAM sector.  An access-policy
+// window marks the buffer the iteration reads as persisting in a set-aside
+// part of L2 (cudaLimitPersistingL2CacheSize); the window follows the double
+// buffer from iteration to iteration.  RIMDP_L2_PERSIST=0 disables it.
+void setup_l2_persistence(rimdp_model* m, size_t value_bytes) {
+    m->l2_persist = 0;
+    const char* e = getenv("RIMDP_L2_PERSIST");
+    if (e && atoi(e) == 0) return;
+    if (value_bytes < (8u << 20)) return; // small V stays in L2 anyway
+    int max_persist = 0;
+    if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, m->device) != cudaSuccess ||
+        max_persist <= 0)
+        return;
+    const size_t want = std::min<size_t>((size_t)max_persist, value_bytes);
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    m->l2_persist = want;
+}
+
+void set_value_window(rimdp_model* m, const void* v, size_t bytes) {
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = const_cast<void*>(v);
+    a.accessPolicyWindow.num_bytes = bytes;
+    a.accessPolicyWindow.hitRatio = std::min(1.0f, (float)m->l2_persist / (float)std::max<size_t>(bytes, 1));
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CK(cudaStreamSetAttribute(m->stream, cudaStreamAttributeAccessPolicyWindow, &a));
+}
+
 // ---------------------------------------------------------------------------
 // Solve loop
 
@@ -394,6 +437,7 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     const long long cap = std::max<long long>(N, m->value_capacity);
     s.v[0].ensure(sizeof(T) * cap);
     s.v[1].ensure(sizeof(T) * cap);
+    setup_l2_persistence(m, sizeof(T) * (size_t)N);
     if (cap > N) {
         CK(cudaMemsetAsync(s.v[0].as<T>() + N, 0, sizeof(T) * (cap - N), m->stream));
         CK(cudaMemsetAsync(s.v[1].as<T>() + N, 0, sizeof(T) * (cap - N), m->stream));
@@ -509,6 +553,55 @@ void launch_medium(rimdp_model* m, int count, const DevBuf& list, const T* V, T*
                                              m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl, work);
 }
 
+template <class T, int SEG>
+void launch_tiny(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl, bool pess) {
+    auto k = pess ? omax_tiny<T, true, SEG> : omax_tiny<T, false, SEG>;
+    static int per_sm[64] = {};
+    const int dev = m->device & 63;
+    if (!per_sm[dev]) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, 256, 0));
+        per_sm[dev] = std::max(per_sm[dev], 1);
+    }
+    const int steps = (count + 32 / SEG - 1) / (32 / SEG);
+    const int blocks = grid_for(steps, 8 * 4, m->sm_count, per_sm[dev]); // >= 4 steps per warp
+    k<<<blocks, 256, 0, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+                                      m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
+}
+
+template <class T, bool P, bool VS>
+void launch_long_v(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
+    auto k = omax_long<T, P, VS>;
+    const size_t smem = VS ? sizeof(T) * (size_t)m->n_global : 0;
+    static int per_sm[64] = {};
+    static size_t configured_smem[64] = {};
+    const int dev = m->device & 63;
+    if (!per_sm[dev] || configured_smem[dev] != smem) {
+        if (VS) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, kWarpsPerBlock * 32, smem));
+        per_sm[dev] = std::max(per_sm[dev], 1);
+        configured_smem[dev] = smem;
+    }
+    const int blocks = grid_for(count, kWarpsPerBlock * kLongGroup, m->sm_count, per_sm[dev]);
+    k<<<blocks, kWarpsPerBlock * 32, smem, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(),
+                                                          m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
+                                                          m->rem.as<T>(), V, m->n_global, q, ctl);
+}
+
+// Exact long columns; the value vector is staged in shared memory when it is
+// small (kLongVsMaxBytes) and the columns are long enough to amortise it.
+template <class T>
+void launch_long(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl, bool pess) {
+    const bool vs = sizeof(T) * (size_t)m->n_global <= (size_t)kLongVsMaxBytes &&
+                    (long long)count * 64 >= (long long)m->n_global;
+    if (pess) {
+        if (vs) launch_long_v<T, true, true>(m, count, list, V, q, ctl);
+        else launch_long_v<T, true, false>(m, count, list, V, q, ctl);
+    } else {
+        if (vs) launch_long_v<T, false, true>(m, count, list, V, q, ctl);
+        else launch_long_v<T, false, false>(m, count, list, V, q, ctl);
+    }
+}
+
 // Per-column expectations q for the columns of one set of class lists.
 template <class T>
 void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
@@ -519,15 +612,12 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
                                                           m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
                                                           m->rem.as<T>(), V, q, ctl, work);
     }
+    if (L.n_tiny[0] > 0) launch_tiny<T, 4>(m, L.n_tiny[0], L.tiny_list[0], V, q, ctl, pess);
+    if (L.n_tiny[1] > 0) launch_tiny<T, 8>(m, L.n_tiny[1], L.tiny_list[1], V, q, ctl, pess);
+    if (L.n_tiny[2] > 0) launch_tiny<T, 16>(m, L.n_tiny[2], L.tiny_list[2], V, q, ctl, pess);
     if (L.n_medium[0] > 0) launch_medium<T, 2>(m, L.n_medium[0], L.medium_list[0], V, q, ctl, pess, work + 2);
     if (L.n_medium[1] > 0) launch_medium<T, 4>(m, L.n_medium[1], L.medium_list[1], V, q, ctl, pess, work + 3);
-    if (L.n_exact > 0) {
-        const int blocks = grid_for(L.n_exact, kWarpsPerBlock * kLongGroup, m->sm_count, 8);
-        auto k = pess ? omax_long<T, true> : omax_long<T, false>;
-        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(L.n_exact, L.exact_list.as<int>(), m->colptr.as<long long>(),
-                                                         m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
-                                                         m->rem.as<T>(), V, q, ctl);
-    }
+    if (L.n_exact > 0) launch_long<T>(m, L.n_exact, L.exact_list, V, q, ctl, pess);
     if (pess)
         launch_sorted<T, true>(m, L, V, q, ctl);
     else
@@ -585,6 +675,7 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
             (T)s.eps, a, ctl);
     }
     if (ev) CK(cudaEventRecord(ev[1], m->stream));
+    if (m->l2_persist) set_value_window(m, vin, sizeof(T) * (size_t)m->n_global);
     launch_columns<T>(m, m->qp, vin, s.q.as<T>(), ctl, s.pess, work);
     if (ev) CK(cudaEventRecord(ev[2], m->stream));
     if (m->nlong_states > 0) {
@@ -598,7 +689,8 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
 
 int kernels_per_iteration(const rimdp_model* m) {
     int k = (m->nbatch > 0) + (m->qp.n_short > 0) + (m->qp.n_exact > 0) + (m->nlong_states > 0) +
-            (m->qp.n_medium[0] > 0) + (m->qp.n_medium[1] > 0);
+            (m->qp.n_medium[0] > 0) + (m->qp.n_medium[1] > 0) + (m->qp.n_tiny[0] > 0) + (m->qp.n_tiny[1] > 0) +
+            (m->qp.n_tiny[2] > 0);
     for (int i = 0; i < kSortedClasses; ++i) k += m->qp.n_sorted[i] > 0;
     return k;
 }
@@ -932,7 +1024,7 @@ int rimdp_model_info_get(rimdp_model* m, rimdp_model_info* o) {
     o->max_column_length = m->maxlen;
     o->num_infeasible_columns = (int)m->infeasible_cols.size();
     o->device_bytes = m->device_bytes;
-    o->short_columns = m->all.n_short;
+    o->short_columns = m->all.n_short + m->all.n_tiny[0] + m->all.n_tiny[1] + m->all.n_tiny[2];
     o->mid_columns = m->all.n_exact + m->all.n_medium[0] + m->all.n_medium[1];
     o->long_columns = m->all.total_sorted();
     return RIMDP_OK;

@@ -287,9 +287,11 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
             for (int nsel = 0; avail > T(0) && nsel < Lc; ++nsel) {
                 const int sel = warp_argmin_sentinel(key);
                 const T gs = __shfl_sync(kFull, gc, sel);
-                if (lane == sel) {
-                    p = N::add(lc, gc < avail ? gc : avail);
-                    key = ~Bits(0);
+                {   // branch-free winner update (a divergent branch costs more than the DADD)
+                    const bool me = lane == sel;
+                    const T pn = N::add(lc, gc < avail ? gc : avail);
+                    p = me ? pn : p;
+                    key = me ? ~Bits(0) : key;
                 }
                 consumed = N::add(consumed, gs);
                 avail = N::sub(r, consumed);
@@ -330,6 +332,109 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
         } else {
             load_meta(nbase);
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Tiny columns (<= SEG entries, SEG = 4, 8 or 16): 32 / SEG columns per warp
+// step, one SEG-lane segment per column (power-law models are dominated by
+// columns of 1-4 entries, which would leave most of omax_short's lanes
+// idle).  Segment reductions use redux/shfl/ballot with the segment's lane
+// mask, so the segments' greedy loops (omax.hpp:98-112) run independently;
+// the expectation is summed sequentially in row order by shuffling the
+// segment's products to its first lane (omax.hpp:169-173): bit-exact.
+// Two-stage pipeline: the next step's metadata and rows are in flight while
+// the current step is reduced.
+template <class T, bool kPess, int SEG>
+__global__ void __launch_bounds__(256)
+omax_tiny(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+          const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+          const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    constexpr int CPW = 32 / SEG;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    const int lane = threadIdx.x & 31, sg = lane / SEG, sl = lane % SEG;
+    const unsigned segmask = (SEG == 32 ? kFull : ((1u << SEG) - 1u)) << (sg * SEG);
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int nsteps = (nlist + CPW - 1) / CPW;
+    const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
+    int step = gw;
+    if (step >= nsteps) return;
+    auto meta = [&](int st, int& c, long long& b, int& L, T& r) {
+        const int idx = st * CPW + sg;
+        c = -1;
+        b = 0;
+        L = 0;
+        r = T(0);
+        if (st < nsteps && idx < nlist) {
+            c = __ldg(list + idx);
+            b = __ldg(colptr + c);
+            L = static_cast<int>(__ldg(colptr + c + 1) - b);
+            r = __ldg(rem + c);
+        }
+    };
+    int c, L;
+    long long b;
+    T r;
+    meta(step, c, b, L, r);
+    int row = sl < L ? ld_hint(rows + b + sl, pstream) : 0;
+    for (;;) {
+        T l = T(0), g = T(0), v = T(0);
+        if (sl < L) {
+            l = ld_hint(lower + b + sl, pstream);
+            g = ld_hint(gap + b + sl, pstream);
+            v = ld_hint(V + row, pval);
+        }
+        const int nstep = step + nw;
+        int c2, L2;
+        long long b2;
+        T r2;
+        meta(nstep, c2, b2, L2, r2);
+        const int row2 = sl < L2 ? ld_hint(rows + b2 + sl, pstream) : 0;
+        // greedy of this segment's column.  The loop is warp-uniform (segments
+        // that are done idle through it) and every collective uses the full
+        // mask: per-segment masks in divergent code serialise per segment.
+        Bits key = sl < L ? order_key<T>(v, kPess) : ~Bits(0);
+        T p = l, consumed = T(0), avail = r;
+        int nsel = 0;
+        for (;;) {
+            const bool active = avail > T(0) && nsel < L;
+            if (!__any_sync(kFull, active)) break;
+            // segment minimum of the key: xor butterfly inside the segment
+            Bits mk = key;
+#pragma unroll
+            for (int o = SEG / 2; o > 0; o >>= 1) {
+                const Bits y = __shfl_xor_sync(kFull, mk, o);
+                mk = y < mk ? y : mk;
+            }
+            const int sel = __ffs(__ballot_sync(kFull, key == mk) & segmask) - 1; // lowest lane = lowest position
+            const T gs = __shfl_sync(kFull, g, sel < 0 ? lane : sel);
+            if (active) {
+                if (lane == sel) {
+                    p = N::add(l, g < avail ? g : avail);
+                    key = ~Bits(0);
+                }
+                consumed = N::add(consumed, gs);
+                avail = N::sub(r, consumed);
+                ++nsel;
+            }
+        }
+        const T x = sl < L ? N::mul(v, p) : T(0);
+        const int maxL = __reduce_max_sync(kFull, static_cast<unsigned>(L));
+        T acc = T(0);
+        for (int i = 0; i < maxL; ++i) {
+            const T y = __shfl_sync(kFull, x, sg * SEG + (i < SEG ? i : 0));
+            if (i < L) acc = N::add(acc, y);
+        }
+        if (sl == 0 && c >= 0) q[c] = acc;
+        step = nstep;
+        if (step >= nsteps) break;
+        c = c2;
+        b = b2;
+        L = L2;
+        r = r2;
+        row = row2;
     }
 }
 
@@ -554,7 +659,7 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
 // lane j adds column j's 32 products to its running sum — sequentially in
 // row order, so bit-exact (omax.hpp:169-173), with the group's sums advancing
 // in parallel instead of one lane summing one column.
-constexpr int kLongTopK = 4;
+constexpr int kLongTopK = 2;
 constexpr int kLongGroup = 8;
 
 template <class T>
@@ -566,17 +671,30 @@ struct LongCut {
     T pval[kMaxPartial];
 };
 
-template <class T, bool kPess>
+// kVs: the whole value vector (nv entries) is staged in shared memory once
+// per block and gathered from there (small models, e.g. config 3's 2000
+// states), instead of from L1/L2 where the column stream keeps evicting it.
+constexpr int kLongVsMaxBytes = 64 * 1024;
+
+template <class T, bool kPess, bool kVs>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
           const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
-          const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, Ctl* __restrict__ ctl) {
+          const T* __restrict__ rem, const T* __restrict__ Vg, int nv, T* __restrict__ q, Ctl* __restrict__ ctl) {
     using N = Num<T>;
     using Bits = typename N::Bits;
     constexpr int K = kLongTopK, U = 4, G = kLongGroup;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     __shared__ T xs[kWarpsPerBlock][G][33];
     __shared__ LongCut<T> cuts[kWarpsPerBlock][G];
+    extern __shared__ __align__(16) unsigned char vs_raw[];
+    const T* __restrict__ V = Vg;
+    if constexpr (kVs) {
+        T* vs = reinterpret_cast<T*>(vs_raw);
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) vs[i] = __ldg(Vg + i);
+        __syncthreads();
+        V = vs;
+    }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
     for (int base = gw * G; base < nlist; base += nw * G) {
@@ -617,7 +735,7 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int j = j0 + u * 32 + lane;
-                    vv[u] = j < L ? __ldg(V + rw[u]) : T(0);
+                    vv[u] = j < L ? V[rw[u]] : T(0);
                     gg[u] = j < L ? __ldg(gap + b + j) : T(0);
                 }
 #pragma unroll
@@ -702,7 +820,7 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
                     int bp = INT_MAX;
                     bool have = false;
                     for (int j = lane; j < L; j += 32) {
-                        const Bits k = N::key(__ldg(V + __ldg(rows + b + j)), kPess);
+                        const Bits k = N::key(V[__ldg(rows + b + j)], kPess);
                         const bool after = !any || k > lastk || (k == lastk && j > lastp);
                         if (after && (!have || k < bk || (k == bk && j < bp))) {
                             bk = k;
@@ -757,7 +875,7 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
                 const long long b = __shfl_sync(kFull, mbeg, jc);
                 const int L = __shfl_sync(kFull, mlen, jc);
                 if (jc < ng && j < L) {
-                    const T v = __ldg(V + rw[jc]);
+                    const T v = V[rw[jc]];
                     const T l = __ldg(lower + b + j);
                     const LongCut<T>& cu = cuts[w][jc];
                     T p = l;
@@ -962,48 +1080,54 @@ omax_sorted(int nlist, const int* __restrict__ list, const long long* __restrict
 }
 
 // ---------------------------------------------------------------------------
-// Long columns with many greedy picks (33 .. 8192 entries): weighted
-// quickselect of the greedy's cut instead of a full sort.
+// Long columns with many greedy picks (33 .. 8192 entries): selection of the
+// greedy's cut over per-thread sorted runs, instead of a full sort.
 //
 // The greedy (omax.hpp:98-112) gives every position before the cut c its
 // full gap, c the rest of the remainder and every later position nothing,
-// where c is the last position (in the adversary order) whose prefix gap
-// sum F(c) = sum of the gaps ordered before it is < rem.  So only c and
-// F(c) are needed, not the order itself.  They are found by quickselect on
-// the composite key (order key of V[row], position): each pass splits the
-// candidate set at a pivot element into Left (< pivot) and Right (>= pivot),
-// one group-wide reduction yields the Left gap sum; if base + sum(Left) <
-// rem the cut is in Right (base += sum(Left)), otherwise in Left.  The next
-// pivot is the candidate of the chosen side with the smallest pseudo-random
-// priority h(pos) = pos * 0x9E3779B1 mod 2^13 (a bijection, so the position
-// is recovered from the reduced minimum).  Expected passes ~ 2 ln L (a
-// random BST's depth): ~8 at L = 64, ~17 at L = 4096, against log2(L)^2 / 2
-// barrier stages for a bitonic sort.
+// where c is the last position (in the adversary order of (V[row], row)) whose
+// prefix gap sum F(c) < rem.  So the expectation is
+//     q = sum_i V_i l_i + sum_{i before c} V_i g_i + V_c min(g_c, rem - F(c))
+// and only c and F(c) are needed, not the order itself.
 //
-// Work unit: one warp per column (NT = 32: no barriers) up to 512 entries,
-// one CTA per column (NT = 256 / 512: one barrier per pass, partials double
-// buffered) beyond.  Thread t of the group owns positions e * NT + t, so
-// every load is coalesced.  Gap sums are in tree order, so, like
-// omax_sorted, results are within a few ulps of the reference (tests bound
-// them by 1e-12 per step); deterministic.
+// Work unit: a group of NT threads per column, E = 2..8 entries per thread
+// (thread t owns positions e * NT + t: coalesced loads).  Each thread sorts
+// its E entries by (order key, position) in registers (bitonic network) and
+// publishes the sorted run to shared memory with exclusive prefix sums of g
+// and of V g.  Selection passes: every thread keeps a candidate index range
+// [lo, hi) of its run; a pivot P splits each range by one binary search, a
+// group reduction adds the gap mass below P (differences of the run
+// prefixes) and decides the side holding c (base + mass < rem: c >= P); the
+// next pivot is the median of the largest remaining range, so each pass
+// roughly halves the candidates: about log2(L) passes of O(log E) work per
+// thread, against a full sort's log2(L)^2 / 2 barrier stages.
+//
+// Groups of NT = 32 (up to 256 entries) are warps: reductions by shuffles
+// only.  Larger columns take one CTA (NT = 64 .. 1024): one barrier per pass,
+// warp partials double-buffered.  The sums run in a different order than
+// the reference's sequential loops, so results are within a few ulps of it
+// (tests bound them by 1e-12 per step); deterministic.
 template <int LG>
 struct SelectShape {
-    // LG = ceil(log2(max entries)): 6..9 warp per column, 10..13 CTA per column
-    static constexpr int NT = LG <= 9 ? 32 : (LG <= 12 ? 256 : 512);
-    static constexpr int E = (1 << LG) / NT;
-    static constexpr int Block = NT == 32 ? 256 : NT;
-    static constexpr int Groups = Block / NT;
+    static constexpr int Len = 1 << LG;
+    static constexpr int E = 8;                        // entries per thread
+    static constexpr int LogE = 3;
+    static constexpr int NT = Len / E;                 // threads per column: 8 .. 1024
+    static constexpr int Block = NT < 32 ? 256 : NT;
+    static constexpr int Groups = Block / NT;          // columns per block
+    static constexpr int NW = NT > 32 ? NT / 32 : 1;   // warps per column
+    template <class T>
+    static constexpr size_t group_bytes() {
+        // keys, (E+1) x NT prefix sums of g and of V g, u16 positions
+        return ((size_t)Len * sizeof(typename Num<T>::Bits) + 2 * sizeof(T) * (size_t)(Len + NT) +
+                2 * (size_t)Len + 15) / 16 * 16;
+    }
     template <class T>
     static constexpr size_t smem() {
-        // keys (8 B per entry, either dtype) + CTA partials: 2 x NW sums, 8 x NW words
-        return Groups * (1 << LG) * 8 + (NT == 32 ? 0 : (NT / 32) * (2 * sizeof(T) + 32));
+        // CTA columns: per-warp partials (sum, count, two pivot proposals) + the decision
+        return Groups * group_bytes<T>() + (NW > 1 ? NW * (sizeof(T) + 16) + 32 : 0);
     }
 };
-
-constexpr unsigned kSelMul = 0x9E3779B1u, kSelInv = 0x0E8B2F51u; // kSelMul * kSelInv == 1 mod 2^32
-constexpr unsigned kSelMask = (1u << 13) - 1;
-__device__ __forceinline__ unsigned sel_hash(unsigned pos) { return (pos * kSelMul) & kSelMask; }
-__device__ __forceinline__ unsigned sel_unhash(unsigned h) { return (h * kSelInv) & kSelMask; }
 
 template <class T>
 __device__ __forceinline__ T value_of_key(typename Num<T>::Bits k, bool pess) {
@@ -1016,6 +1140,55 @@ __device__ __forceinline__ T value_of_key(typename Num<T>::Bits k, bool pess) {
     return v;
 }
 
+// Pivot proposal: (range length, permuted thread, index of the range
+// median), compared as one integer so that a max-reduction picks the largest
+// range; ties between equal lengths (late passes: ranges of one entry) go to
+// a pass-dependent pseudo-random thread, so the pivot stays a random
+// candidate instead of degenerating to an extreme one.
+__device__ __forceinline__ unsigned sel_perm(int t, int pass) {
+    return ((static_cast<unsigned>(t) + static_cast<unsigned>(pass) * 158u) * 757u) & 1023u;
+}
+__device__ __forceinline__ int sel_unperm(unsigned x, int pass) {
+    return static_cast<int>((x * 349u - static_cast<unsigned>(pass) * 158u) & 1023u); // 757 * 349 = 1 mod 1024
+}
+__device__ __forceinline__ unsigned sel_pack(int n, int t, int mid, int pass) {
+    return n > 0 ? (static_cast<unsigned>(n) << 14) | (sel_perm(t, pass) << 4) | static_cast<unsigned>(mid) : 0u;
+}
+
+// Reductions over the lanes of a segment of S <= 32 lanes: xor butterflies
+// with offsets < S stay inside the segment, so they run with the full mask
+// (per-segment masks would serialise per segment); sums in a fixed tree
+// order, so deterministic.
+template <int S, class T>
+__device__ __forceinline__ T seg_sum(T x) {
+#pragma unroll
+    for (int o = S / 2; o > 0; o >>= 1) x = Num<T>::add(x, __shfl_xor_sync(kFull, x, o));
+    return x;
+}
+template <int S>
+__device__ __forceinline__ unsigned seg_addu(unsigned x) {
+    if constexpr (S == 32) {
+        return __reduce_add_sync(kFull, x);
+    } else {
+#pragma unroll
+        for (int o = S / 2; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+        return x;
+    }
+}
+template <int S>
+__device__ __forceinline__ unsigned seg_maxu(unsigned x) {
+    if constexpr (S == 32) {
+        return __reduce_max_sync(kFull, x);
+    } else {
+#pragma unroll
+        for (int o = S / 2; o > 0; o >>= 1) {
+            const unsigned y = __shfl_xor_sync(kFull, x, o);
+            x = y > x ? y : x;
+        }
+        return x;
+    }
+}
+
 template <class T, bool kPess, int LG>
 __global__ void __launch_bounds__(SelectShape<LG>::Block)
 omax_select(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
@@ -1024,170 +1197,228 @@ omax_select(int nlist, const int* __restrict__ list, const long long* __restrict
     using N = Num<T>;
     using Bits = typename N::Bits;
     using Sh = SelectShape<LG>;
-    constexpr int NT = Sh::NT, E = Sh::E, NW = NT / 32;
+    constexpr int E = Sh::E, NT = Sh::NT, NW = Sh::NW, LOGE = Sh::LogE;
+    constexpr int S = NT < 32 ? NT : 32; // lanes of one column inside a warp
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int grp = threadIdx.x / NT, t = threadIdx.x % NT, wig = t >> 5;
-    Bits* skey = reinterpret_cast<Bits*>(smem_raw) + grp * (1 << LG);
-    // CTA groups: per-warp partials, double buffered by pass parity
-    T* ps = reinterpret_cast<T*>(smem_raw + Sh::Groups * (1 << LG) * 8);
-    unsigned* pu = reinterpret_cast<unsigned*>(ps + 2 * NW); // [0, NW): first pivot; [2 NW, 8 NW): passes
+    unsigned char* gb = smem_raw + grp * Sh::template group_bytes<T>();
+    Bits* rk = reinterpret_cast<Bits*>(gb);                       // [E][NT] sorted keys
+    T* rpre = reinterpret_cast<T*>(gb + Sh::Len * sizeof(Bits)); // [E+1][NT] exclusive prefix of g
+    T* rvg = rpre + (Sh::Len + NT);                               // [E+1][NT] exclusive prefix of V g
+    unsigned short* rp = reinterpret_cast<unsigned short*>(rvg + (Sh::Len + NT)); // [E][NT] positions
+    // CTA columns: warp partials and the decision of warp 0
+    T* psl = reinterpret_cast<T*>(smem_raw + Sh::Groups * Sh::template group_bytes<T>());
+    unsigned* pu = reinterpret_cast<unsigned*>(psl + NW);           // [NW][3]: count, packL, packR
+    T* dbase = reinterpret_cast<T*>(pu + ((3 * NW + 1) & ~1));      // decision: base (8-byte aligned)
+    unsigned* dword = reinterpret_cast<unsigned*>(dbase + 1);      // decision: side, ncand, pack
     const int ngroups = gridDim.x * Sh::Groups;
+    const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
 
-    for (int item = blockIdx.x * Sh::Groups + grp; item < nlist; item += ngroups) {
-        const int c = __ldg(list + item);
-        const long long b = __ldg(colptr + c);
-        const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
-        const T r = __ldg(rem + c);
+    for (int item0 = blockIdx.x * Sh::Groups; item0 < nlist; item0 += ngroups) {
+        const int item = item0 + grp;
+        const bool live = item < nlist;
+        int L = 0;
+        long long b = 0;
+        T r = T(0);
+        int c = -1;
+        if (live) {
+            c = __ldg(list + item);
+            b = __ldg(colptr + c);
+            L = static_cast<int>(__ldg(colptr + c + 1) - b);
+            r = __ldg(rem + c);
+        }
+        // ---- load this thread's entries; sum of V l ----
         int rw[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int pos = e * NT + t;
-            rw[e] = pos < L ? __ldg(rows + b + pos) : 0;
+            rw[e] = pos < L ? ld_hint(rows + b + pos, pstream) : 0;
         }
-        Bits key[E];
+        Bits k[E];
+        int p[E];
         T g[E];
-        unsigned cand = 0;
-        unsigned hmin = 0xffffffffu;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int pos = e * NT + t;
-            key[e] = ~Bits(0);
-            g[e] = T(0);
-            if (pos < L) {
-                key[e] = order_key<T>(__ldg(V + rw[e]), kPess);
-                g[e] = __ldg(gap + b + pos);
-                cand |= 1u << e;
-                const unsigned h = sel_hash(static_cast<unsigned>(pos));
-                hmin = h < hmin ? h : hmin;
-            }
-            skey[pos] = key[e];
-        }
-        // first pivot: the valid position with the smallest priority
-        hmin = __reduce_min_sync(kFull, hmin);
-        if constexpr (NW > 1) {
-            if (lane == 0) pu[wig] = hmin;
-            __syncthreads();
-            hmin = pu[0];
-#pragma unroll
-            for (int i = 1; i < NW; ++i) hmin = pu[i] < hmin ? pu[i] : hmin;
-            __syncthreads();
-        } else {
-            __syncwarp();
-        }
-        int pp = static_cast<int>(sel_unhash(hmin));
-        Bits pk = skey[pp];
-        T base = T(0);
-        int ncand = L;
-        int cpos = -1; // the cut position (none when rem <= 0)
-        Bits ckey = 0;
-        if (r > T(0)) {
-            for (int pass = 0;; ++pass) {
-                T sl = T(0);
-                int nl = 0;
-                unsigned hl = 0xffffffffu, hr = 0xffffffffu, lm = 0;
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    if (cand >> e & 1u) {
-                        const int pos = e * NT + t;
-                        const bool lt = key[e] < pk || (key[e] == pk && pos < pp);
-                        const unsigned h = sel_hash(static_cast<unsigned>(pos));
-                        if (lt) {
-                            sl = N::add(sl, g[e]);
-                            ++nl;
-                            lm |= 1u << e;
-                            hl = h < hl ? h : hl;
-                        } else if (pos != pp) {
-                            hr = h < hr ? h : hr;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sl = N::add(sl, __shfl_xor_sync(kFull, sl, o));
-                nl = static_cast<int>(__reduce_add_sync(kFull, static_cast<unsigned>(nl)));
-                hl = __reduce_min_sync(kFull, hl);
-                hr = __reduce_min_sync(kFull, hr);
-                if constexpr (NW > 1) {
-                    const int buf = pass & 1;
-                    if (lane == 0) {
-                        ps[buf * NW + wig] = sl;
-                        pu[2 * NW + (buf * NW + wig) * 3 + 0] = static_cast<unsigned>(nl);
-                        pu[2 * NW + (buf * NW + wig) * 3 + 1] = hl;
-                        pu[2 * NW + (buf * NW + wig) * 3 + 2] = hr;
-                    }
-                    __syncthreads();
-                    sl = ps[buf * NW];
-                    nl = static_cast<int>(pu[2 * NW + buf * NW * 3]);
-                    hl = pu[2 * NW + buf * NW * 3 + 1];
-                    hr = pu[2 * NW + buf * NW * 3 + 2];
-#pragma unroll
-                    for (int i = 1; i < NW; ++i) {
-                        sl = N::add(sl, ps[buf * NW + i]);
-                        nl += static_cast<int>(pu[2 * NW + (buf * NW + i) * 3]);
-                        const unsigned a = pu[2 * NW + (buf * NW + i) * 3 + 1];
-                        const unsigned z = pu[2 * NW + (buf * NW + i) * 3 + 2];
-                        hl = a < hl ? a : hl;
-                        hr = z < hr ? z : hr;
-                    }
-                }
-                if (N::add(base, sl) < r) { // the cut is in Right (>= pivot)
-                    base = N::add(base, sl);
-                    cand &= ~lm;
-                    ncand -= nl;
-                    if (ncand == 1) {
-                        cpos = pp;
-                        ckey = pk;
-                        break;
-                    }
-                    pp = static_cast<int>(sel_unhash(hr));
-                } else { // the cut is in Left
-                    cand &= lm;
-                    ncand = nl;
-                    if (ncand == 1) {
-                        cpos = static_cast<int>(sel_unhash(hl));
-                        ckey = skey[cpos];
-                        break;
-                    }
-                    pp = static_cast<int>(sel_unhash(hl));
-                }
-                pk = skey[pp];
-            }
-        }
-        // expectation: positions before the cut take lower + gap, the cut
-        // lower + min(gap, rem - F(cut)), the rest lower (tree order sum)
-        const T availc = N::sub(r, base);
         T acc = T(0);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int pos = e * NT + t;
+            k[e] = ~Bits(0);
+            p[e] = 0xffff;
+            g[e] = T(0);
             if (pos < L) {
-                const T l = __ldg(lower + b + pos);
-                T p = l;
-                if (cpos >= 0) {
-                    if (pos == cpos)
-                        p = N::add(l, g[e] < availc ? g[e] : availc);
-                    else if (key[e] < ckey || (key[e] == ckey && pos < cpos))
-                        p = N::add(l, g[e]);
-                }
-                acc = N::add(acc, N::mul(value_of_key<T>(key[e], kPess), p));
+                const T v = ld_hint(V + rw[e], pval);
+                k[e] = order_key<T>(v, kPess);
+                p[e] = pos;
+                g[e] = ld_hint(gap + b + pos, pstream);
+                acc = N::add(acc, N::mul(v, ld_hint(lower + b + pos, pstream)));
             }
         }
+        const int cnt = min(E, max(0, (L - t + NT - 1) / NT));
+        // ---- sort the run by (key, position): bitonic network in registers ----
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc = N::add(acc, __shfl_xor_sync(kFull, acc, o));
+        for (int size = 2; size <= E; size <<= 1) {
+#pragma unroll
+            for (int stride = size / 2; stride > 0; stride >>= 1) {
+#pragma unroll
+                for (int i = 0; i < E; ++i) {
+                    const int j = i ^ stride;
+                    if (j > i) {
+                        const bool up = (i & size) == 0;
+                        const bool gt = k[i] > k[j] || (k[i] == k[j] && p[i] > p[j]);
+                        if (gt == up) {
+                            const Bits tk = k[i];
+                            k[i] = k[j];
+                            k[j] = tk;
+                            const int tp = p[i];
+                            p[i] = p[j];
+                            p[j] = tp;
+                            const T tg = g[i];
+                            g[i] = g[j];
+                            g[j] = tg;
+                        }
+                    }
+                }
+            }
+        }
+        {
+            T sg = T(0), svg = T(0);
+            rpre[t] = sg;
+            rvg[t] = svg;
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                rk[i * NT + t] = k[i];
+                rp[i * NT + t] = static_cast<unsigned short>(p[i]);
+                if (i < cnt) {
+                    sg = N::add(sg, g[i]);
+                    svg = N::add(svg, N::mul(value_of_key<T>(k[i], kPess), g[i]));
+                }
+                rpre[(i + 1) * NT + t] = sg;
+                rvg[(i + 1) * NT + t] = svg;
+            }
+        }
+        // ---- selection of the cut ----
+        int lo = 0, hi = cnt;
+        unsigned pack = seg_maxu<S>(sel_pack(cnt, t, cnt / 2, 0));
         if constexpr (NW > 1) {
-            // partial slots of pass parity 0/1 are free again only after a barrier
+            if (lane == 0) pu[wig] = pack;
             __syncthreads();
-            if (lane == 0) ps[wig] = acc;
+            pack = pu[0];
+#pragma unroll
+            for (int i = 1; i < NW; ++i) pack = pu[i] > pack ? pu[i] : pack;
+            __syncthreads();
+        } else {
+            __syncwarp();
+        }
+        T base = T(0);
+        const bool picks = live && r > T(0);
+        // segment columns: the pass loop is warp-uniform (done segments idle
+        // through it), so every collective runs convergent with the full mask
+        bool act = picks;
+        int ncand = L;
+        if (NW > 1 ? picks : __any_sync(kFull, act)) {
+            for (int pass = 0;; ++pass) {
+                // (a segment that is done idles on its own first entry)
+                const int ts = act ? sel_unperm((pack >> 4) & 1023u, pass) : t;
+                const int ms = act ? static_cast<int>(pack & 15u) : 0;
+                const Bits pk = rk[ms * NT + ts];
+                const int pp = rp[ms * NT + ts];
+                // first index of [lo, hi) with (key, pos) >= (pk, pp)
+                int i0 = lo, i1 = hi;
+#pragma unroll
+                for (int st = 0; st <= LOGE; ++st) {
+                    if (i0 < i1) {
+                        const int m = (i0 + i1) >> 1;
+                        const Bits km = rk[m * NT + t];
+                        const int pm = rp[m * NT + t];
+                        if (km < pk || (km == pk && pm < pp)) i0 = m + 1;
+                        else i1 = m;
+                    }
+                }
+                const int split = i0;
+                T sl = lo < split ? N::sub(rpre[split * NT + t], rpre[lo * NT + t]) : T(0);
+                int nl = split - lo;
+                const bool ownsP = t == ts && split < hi && split == ms;
+                const int rs = split + (ownsP ? 1 : 0);
+                unsigned packL = sel_pack(nl, t, lo + nl / 2, pass + 1);
+                unsigned packR = sel_pack(hi - rs, t, rs + (hi - rs) / 2, pass + 1);
+                sl = seg_sum<S>(sl);
+                nl = static_cast<int>(seg_addu<S>(static_cast<unsigned>(nl)));
+                packL = seg_maxu<S>(packL);
+                packR = seg_maxu<S>(packR);
+                bool right;
+                if constexpr (NW > 1) {
+                    if (lane == 0) {
+                        psl[wig] = sl;
+                        pu[3 * wig + 0] = static_cast<unsigned>(nl);
+                        pu[3 * wig + 1] = packL;
+                        pu[3 * wig + 2] = packR;
+                    }
+                    __syncthreads();
+                    if (wig == 0) {
+                        // warp 0 combines the warp partials and decides
+                        T ws = lane < NW ? psl[lane] : T(0);
+                        ws = seg_sum<32>(ws);
+                        const unsigned wn = __reduce_add_sync(kFull, lane < NW ? pu[3 * lane] : 0u);
+                        const unsigned wl = __reduce_max_sync(kFull, lane < NW ? pu[3 * lane + 1] : 0u);
+                        const unsigned wr = __reduce_max_sync(kFull, lane < NW ? pu[3 * lane + 2] : 0u);
+                        if (lane == 0) {
+                            const bool rt = N::add(base, ws) < r;
+                            dbase[0] = rt ? N::add(base, ws) : base;
+                            dword[0] = rt;
+                            dword[1] = static_cast<unsigned>(rt ? ncand - static_cast<int>(wn) : static_cast<int>(wn));
+                            dword[2] = rt ? wr : wl;
+                        }
+                    }
+                    __syncthreads();
+                    right = dword[0] != 0;
+                    base = dbase[0];
+                    ncand = static_cast<int>(dword[1]);
+                    pack = dword[2];
+                    if (right) lo = split;
+                    else hi = split;
+                    if (ncand <= 1) break;
+                } else {
+                    right = N::add(base, sl) < r; // the cut is at or after the pivot
+                    if (act) {
+                        if (right) {
+                            base = N::add(base, sl);
+                            ncand -= nl;
+                            pack = packR;
+                            lo = split;
+                        } else {
+                            ncand = nl;
+                            pack = packL;
+                            hi = split;
+                        }
+                        act = ncand > 1;
+                    }
+                    if (!__any_sync(kFull, act)) break;
+                }
+            }
+        }
+        // ---- expectation: sum V l + sum_{before c} V g + V_c min(g_c, rem - F(c)) ----
+        if (picks) {
+            acc = N::add(acc, rvg[lo * NT + t]);
+            if (hi - lo == 1) { // this thread owns the cut
+                const T vc = value_of_key<T>(rk[lo * NT + t], kPess);
+                const T gc = __ldg(gap + b + rp[lo * NT + t]);
+                const T avail = N::sub(r, base);
+                acc = N::add(acc, N::mul(vc, gc < avail ? gc : avail));
+            }
+        }
+        acc = seg_sum<S>(acc);
+        if constexpr (NW > 1) {
+            if (lane == 0) psl[wig] = acc;
             __syncthreads();
             if (t == 0) {
-                T s = ps[0];
-                for (int i = 1; i < NW; ++i) s = N::add(s, ps[i]);
-                q[c] = s;
+                T s2 = psl[0];
+                for (int i = 1; i < NW; ++i) s2 = N::add(s2, psl[i]);
+                q[c] = s2;
             }
             __syncthreads();
         } else {
-            if (lane == 0) q[c] = acc;
+            if (t == 0 && live) q[c] = acc;
             __syncwarp();
         }
     }
@@ -1481,9 +1712,11 @@ bellman_short(int nbatch, const int* __restrict__ slots, const int2* __restrict_
                 for (int nsel = 0; avail > T(0) && nsel < Lc; ++nsel) {
                     const int sel = warp_argmin_sentinel(key);
                     const T gs = __shfl_sync(kFull, gc, sel);
-                    if (lane == sel) {
-                        p = N::add(lc, gc < avail ? gc : avail);
-                        key = ~Bits(0);
+                    {
+                        const bool me = lane == sel;
+                        const T pn = N::add(lc, gc < avail ? gc : avail);
+                        p = me ? pn : p;
+                        key = me ? ~Bits(0) : key;
                     }
                     consumed = N::add(consumed, gs);
                     avail = N::sub(r, consumed);
