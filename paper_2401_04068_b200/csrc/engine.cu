@@ -147,7 +147,9 @@ struct rimdp_model {
     long long device_bytes = 0;
     int sm_count = 148;
     int short_blocks_per_sm = 4;
-    bool bitonic = false;                     // many-pick long columns: bitonic sort instead of quickselect
+    bool bitonic = false;                     // many-pick long columns: bitonic sort instead of selection
+    bool bucket = true;                       // columns > 256 entries: value buckets first (RIMDP_BUCKET=0: off)
+    DevBuf fallback;                          // [count, columns...] for omax_bucket -> omax_select
     size_t l2_persist = 0;                    // bytes of L2 set aside for the value vector (0: none)
     SolveState s;
 };
@@ -192,7 +194,7 @@ void upload_list(rimdp_model* m, DevBuf& buf, const std::vector<U>& v) {
 
 // Routing mode for long columns (tests): RIMDP_LONG=exact (every long column
 // on the exact warp kernel), sorted (every one on the bitonic CTA kernel),
-// select (every one on the quickselect kernels).
+// select (every one on the selection kernels, no value buckets).
 int long_mode() {
     const char* e = getenv("RIMDP_LONG");
     if (!e) return 0;
@@ -277,6 +279,11 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     }
     const int mode = long_mode();
     m->bitonic = mode == 2;
+    {
+        // RIMDP_LONG=select (tests) keeps every many-pick column on the selection kernels
+        const char* eb = getenv("RIMDP_BUCKET");
+        m->bucket = !(eb && atoi(eb) == 0) && mode != 3;
+    }
     std::vector<signed char> cls(m->ncols);
     std::vector<int> allc(m->ncols), qc;
     int maxlen = 0;
@@ -503,7 +510,8 @@ void launch_sorted_class(rimdp_model* m, int count, const DevBuf& list, const T*
 }
 
 template <class T, bool P, int LG>
-void launch_select_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
+void launch_select_class(rimdp_model* m, int count, const int* list, const T* V, T* q, Ctl* ctl,
+                         const int* count_dev = nullptr) {
     using Sh = SelectShape<LG>;
     auto k = omax_select<T, P, LG>;
     const size_t smem = Sh::template smem<T>();
@@ -517,8 +525,36 @@ void launch_select_class(rimdp_model* m, int count, const DevBuf& list, const T*
         configured[dev] = true;
     }
     const int blocks = grid_for(count, Sh::Groups, m->sm_count, per_sm[dev]);
-    k<<<blocks, Sh::Block, smem, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
-                                              m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
+    k<<<blocks, Sh::Block, smem, m->stream>>>(count, list, m->colptr.as<long long>(), m->rows.as<int>(),
+                                              m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl,
+                                              count_dev);
+}
+
+// Columns of more than 256 entries: value-bucket kernel, then the selection
+// kernel over the columns it could not bracket tightly (fallback list).
+template <class T, bool P, int LG>
+void launch_bucket_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
+    using Sh = BucketShape<LG>;
+    auto k = omax_bucket<T, P, LG>;
+    const size_t smem = Sh::template smem<T>();
+    static bool configured[64] = {};
+    static int per_sm[64] = {};
+    const int dev = m->device & 63;
+    if (!configured[dev]) {
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, Sh::NT, smem));
+        per_sm[dev] = std::max(per_sm[dev], 1);
+        configured[dev] = true;
+    }
+    m->fallback.ensure(sizeof(int) * (size_t)(std::max(count, 1) + 1));
+    int* nfb = m->fallback.as<int>();
+    int* fb = nfb + 1;
+    CK(cudaMemsetAsync(nfb, 0, sizeof(int), m->stream));
+    const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
+    k<<<blocks, Sh::NT, smem, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+                                           m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V,
+                                           q, ctl, fb, nfb);
+    launch_select_class<T, P, LG>(m, count, fb, V, q, ctl, nfb);
 }
 
 // Many-pick long columns by size class: weighted quickselect (omax_select,
@@ -530,8 +566,10 @@ void launch_sorted(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* 
         if (L.n_sorted[i] > 0) {
             if (m->bitonic)
                 launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+            else if (LG >= 9 && m->bucket)
+                launch_bucket_class<T, P, (LG >= 9 ? LG : 9)>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else
-                launch_select_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+                launch_select_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i].as<int>(), V, q, ctl);
         }
         launch_sorted<T, P, LG + 1>(m, L, V, q, ctl);
     }

@@ -1193,10 +1193,12 @@ template <class T, bool kPess, int LG>
 __global__ void __launch_bounds__(SelectShape<LG>::Block)
 omax_select(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
-            const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl) {
+            const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl,
+            const int* __restrict__ nlist_dev) {
     using N = Num<T>;
     using Bits = typename N::Bits;
     using Sh = SelectShape<LG>;
+    if (nlist_dev) nlist = *nlist_dev; // fallback list of omax_bucket
     constexpr int E = Sh::E, NT = Sh::NT, NW = Sh::NW, LOGE = Sh::LogE;
     constexpr int S = NT < 32 ? NT : 32; // lanes of one column inside a warp
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
@@ -1421,6 +1423,336 @@ omax_select(int nlist, const int* __restrict__ list, const long long* __restrict
             if (t == 0 && live) q[c] = acc;
             __syncwarp();
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Long many-pick columns (257 .. 8192 entries), O(L) path: value buckets.
+//
+// One CTA per column, thread t owning positions e * NT + t (E = 8).  With w
+// the value in adversary order (V pessimistic, -V optimistic), the column's
+// entries are cut into B equal-width buckets of [w_min, w_max]: the bucket
+// index is a monotone function of w, so buckets are contiguous in the
+// adversary order and ties share a bucket.  Gap mass per bucket is
+// accumulated in shared memory as fixed-point integers (g * Sc truncated,
+// Sc = 2^31 / (L * max gap): no overflow; integer atomics, deterministic).
+// Since truncation loses < 1 unit per entry, the exact mass before bucket b
+// lies in [F_b, F_b + N_b) (fixed mass and count before b), which brackets the
+// bucket of the cut c (the last entry whose prefix gap mass is < rem) in
+// [b_lo, b_hi]:  b_lo = last non-empty bucket with F_b + N_b <= rem * Sc
+// (certainly reached), b_hi = last non-empty bucket with F_b < rem * Sc.
+// Entries below b_lo are before c: their exact gap sum (double, tree order)
+// is the base, and their V g is added to the expectation.  The <= kBucketCap
+// entries of [b_lo, b_hi] are resolved exactly by warp 0: bitonic sort by
+// (order key, position), exclusive prefix of the gaps from the base, the cut
+// is the last entry whose prefix is < rem.
+//   q = sum V l + sum_{before c} V g + V_c min(g_c, rem - F(c))
+// A column whose bracket holds more than kBucketCap entries (heavy ties,
+// clustered values) is appended to a fallback list for omax_select.  Sums are
+// in tree order: within a few ulps of the reference (1e-12 tests).
+constexpr int kBucketCap = 64;
+
+template <int LG>
+struct BucketShape {
+    static constexpr int Len = 1 << LG;
+    static constexpr int E = 8;
+    static constexpr int NT = Len / E;    // 64 .. 1024
+    static constexpr int NW = NT / 32;
+    static constexpr int B = Len / 8 < 512 ? Len / 8 : 512;
+    template <class T>
+    static constexpr size_t smem() {
+        // hist, cnt (u32 x B); candidates (key, pos, g, V) x kBucketCap; partials; decision words
+        return 2 * 4 * B + kBucketCap * (8 + 4 + 2 * sizeof(T)) + NW * 2 * sizeof(T) + 64;
+    }
+};
+
+template <class T, bool kPess, int LG>
+__global__ void __launch_bounds__(BucketShape<LG>::NT)
+omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+            const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+            const T* __restrict__ rem, const T* __restrict__ maxgap, const T* __restrict__ V, T* __restrict__ q,
+            const Ctl* __restrict__ ctl, int* __restrict__ fallback, int* __restrict__ nfallback) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    using Sh = BucketShape<LG>;
+    constexpr int E = Sh::E, NT = Sh::NT, NW = Sh::NW, B = Sh::B, CAP = kBucketCap;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned* hist = reinterpret_cast<unsigned*>(smem_raw);
+    unsigned* hcnt = hist + B;
+    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hcnt + B);
+    T* cg = reinterpret_cast<T*>(ckey + CAP);
+    T* cv = cg + CAP;
+    int* cpos = reinterpret_cast<int*>(cv + CAP);
+    T* pa = reinterpret_cast<T*>(cpos + CAP);   // [NW] partial A
+    T* pb = pa + NW;                            // [NW] partial B
+    int* dw = reinterpret_cast<int*>(pb + NW);   // decision: b_lo, b_hi, K, ncand counter
+    const int t = threadIdx.x, lane = t & 31, wig = t >> 5;
+    const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
+
+    for (int item = blockIdx.x; item < nlist; item += gridDim.x) {
+        const int c = __ldg(list + item);
+        const long long b = __ldg(colptr + c);
+        const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
+        const T r = __ldg(rem + c);
+        // ---- load; sum V l; range of w ----
+        int rw[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = e * NT + t;
+            rw[e] = pos < L ? ld_hint(rows + b + pos, pstream) : 0;
+        }
+        T v[E], g[E];
+        T acc = T(0);
+        T wlo = T(0), whi = T(0);
+        bool any = false;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = e * NT + t;
+            v[e] = T(0);
+            g[e] = T(0);
+            if (pos < L) {
+                v[e] = ld_hint(V + rw[e], pval);
+                g[e] = ld_hint(gap + b + pos, pstream);
+                acc = N::add(acc, N::mul(v[e], ld_hint(lower + b + pos, pstream)));
+                const T w = kPess ? v[e] : -v[e];
+                wlo = any ? (w < wlo ? w : wlo) : w;
+                whi = any ? (w > whi ? w : whi) : w;
+                any = true;
+            }
+        }
+        for (int i = t; i < 2 * B; i += NT) hist[i] = 0u;
+        if (t == 0) dw[3] = 0;
+        if (!any) { // only threads past the end of a short column
+            wlo = T(1e300);
+            whi = T(-1e300);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T a = __shfl_xor_sync(kFull, wlo, o), z = __shfl_xor_sync(kFull, whi, o);
+            wlo = a < wlo ? a : wlo;
+            whi = z > whi ? z : whi;
+        }
+        if (lane == 0) {
+            pa[wig] = wlo;
+            pb[wig] = whi;
+        }
+        __syncthreads();
+        wlo = pa[0];
+        whi = pb[0];
+#pragma unroll
+        for (int i = 1; i < NW; ++i) {
+            wlo = pa[i] < wlo ? pa[i] : wlo;
+            whi = pb[i] > whi ? pb[i] : whi;
+        }
+        const bool picks = r > T(0);
+        // ---- fixed-point gap histogram over the buckets ----
+        const T span = N::sub(whi, wlo);
+        const T bscale = span > T(0) ? T(B) / span : T(0);
+        const T gm = __ldg(maxgap + c);
+        const double sc = gm > T(0) ? 2147483648.0 / ((double)L * (double)gm) : 0.0;
+        int bk[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = e * NT + t;
+            bk[e] = 0;
+            if (pos < L) {
+                const T w = kPess ? v[e] : -v[e];
+                const int x = static_cast<int>(N::mul(N::sub(w, wlo), bscale));
+                bk[e] = x < B - 1 ? x : B - 1;
+                if (picks) {
+                    atomicAdd(hist + bk[e], static_cast<unsigned>((double)g[e] * sc));
+                    atomicAdd(hcnt + bk[e], 1u);
+                }
+            }
+        }
+        __syncthreads(); // also: partials pa / pb are free again
+        if (!picks) {
+            // no picks: q = sum V l
+        } else {
+            // ---- bracket of the cut's bucket (warp 0) ----
+            if (wig == 0) {
+                constexpr int PB = B / 32 > 0 ? B / 32 : 1;
+                unsigned long long fm = 0;
+                unsigned long long fn = 0;
+                unsigned long long lm[PB], ln[PB];
+#pragma unroll
+                for (int i = 0; i < PB; ++i) {
+                    const int bb = lane * PB + i;
+                    lm[i] = bb < B ? hist[bb] : 0u;
+                    ln[i] = bb < B ? hcnt[bb] : 0u;
+                    fm += lm[i];
+                    fn += ln[i];
+                }
+                // exclusive warp scan of the lane totals
+                unsigned long long em = fm, en = fn;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned long long a = __shfl_up_sync(kFull, em, o), z = __shfl_up_sync(kFull, en, o);
+                    if (lane >= o) {
+                        em += a;
+                        en += z;
+                    }
+                }
+                em -= fm;
+                en -= fn;
+                const double R = (double)r * sc;
+                int blo = -1, bhi = -1;
+#pragma unroll
+                for (int i = 0; i < PB; ++i) {
+                    const int bb = lane * PB + i;
+                    if (ln[i] > 0) {
+                        if ((double)(em + en) <= R) blo = bb;
+                        if ((double)em < R) bhi = bb;
+                    }
+                    em += lm[i];
+                    en += ln[i];
+                }
+                blo = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(blo + 1))) - 1;
+                bhi = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(bhi + 1))) - 1;
+                if (blo < 0) blo = 0; // the first entry is always reached (rem > 0)
+                unsigned k = 0;
+#pragma unroll
+                for (int i = 0; i < PB; ++i) {
+                    const int bb = lane * PB + i;
+                    if (bb >= blo && bb <= bhi) k += static_cast<unsigned>(ln[i]);
+                }
+                k = __reduce_add_sync(kFull, k);
+                if (lane == 0) {
+                    dw[0] = blo;
+                    dw[1] = bhi;
+                    dw[2] = static_cast<int>(k);
+                }
+            }
+            __syncthreads();
+            const int blo = dw[0], bhi = dw[1], K = dw[2];
+            if (K > CAP) {
+                if (t == 0) fallback[atomicAdd(nfallback, 1)] = c;
+                __syncthreads(); // keep dw / hist stable until everyone has read them
+                continue;
+            }
+            // ---- entries before the bracket; candidates to shared memory ----
+            T bs = T(0);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int pos = e * NT + t;
+                if (pos < L) {
+                    if (bk[e] < blo) {
+                        bs = N::add(bs, g[e]);
+                        acc = N::add(acc, N::mul(v[e], g[e]));
+                    } else if (bk[e] <= bhi) {
+                        const int slot = atomicAdd(dw + 3, 1);
+                        ckey[slot] = static_cast<unsigned long long>(order_key<T>(v[e], kPess));
+                        cg[slot] = g[e];
+                        cv[slot] = v[e];
+                        cpos[slot] = pos;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) bs = N::add(bs, __shfl_xor_sync(kFull, bs, o));
+            if (lane == 0) pa[wig] = bs;
+            __syncthreads();
+            if (wig == 0) {
+                T base = pa[0];
+#pragma unroll
+                for (int i = 1; i < NW; ++i) base = N::add(base, pa[i]);
+                // two candidates per lane: index x = j * 32 + lane
+                unsigned long long kk[2];
+                int pp[2];
+                T gg[2], vv[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int x = j * 32 + lane;
+                    const bool ok = x < K;
+                    kk[j] = ok ? ckey[x] : ~0ull;
+                    pp[j] = ok ? cpos[x] : INT_MAX;
+                    gg[j] = ok ? cg[x] : T(0);
+                    vv[j] = ok ? cv[x] : T(0);
+                }
+                // bitonic sort of 64 by (key, pos) ascending
+#pragma unroll
+                for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+                    for (int stride = size / 2; stride > 0; stride >>= 1) {
+                        if (stride == 32) {
+                            // partner in the same lane (j = 0 <-> 1); ascending iff (x & size) == 0
+                            const bool up = (lane & size) == 0; // size == 64: always up
+                            const bool gt = kk[0] > kk[1] || (kk[0] == kk[1] && pp[0] > pp[1]);
+                            if (gt == up) {
+                                const unsigned long long a = kk[0]; kk[0] = kk[1]; kk[1] = a;
+                                const int bp = pp[0]; pp[0] = pp[1]; pp[1] = bp;
+                                const T cgx = gg[0]; gg[0] = gg[1]; gg[1] = cgx;
+                                const T cvx = vv[0]; vv[0] = vv[1]; vv[1] = cvx;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                const int x = j * 32 + lane;
+                                const unsigned long long ok2 = __shfl_xor_sync(kFull, kk[j], stride);
+                                const int op = __shfl_xor_sync(kFull, pp[j], stride);
+                                const T og = __shfl_xor_sync(kFull, gg[j], stride);
+                                const T ov = __shfl_xor_sync(kFull, vv[j], stride);
+                                const bool lower_half = (x & stride) == 0;
+                                const bool up = (x & size) == 0;
+                                // the lower index keeps the smaller when ascending
+                                const bool other_less = ok2 < kk[j] || (ok2 == kk[j] && op < pp[j]);
+                                const bool take = lower_half == up ? other_less : !other_less;
+                                if (take) {
+                                    kk[j] = ok2;
+                                    pp[j] = op;
+                                    gg[j] = og;
+                                    vv[j] = ov;
+                                }
+                            }
+                        }
+                    }
+                }
+                // exclusive prefix of the gaps in sorted order (x = j * 32 + lane)
+                T ex[2];
+                T tot0 = T(0);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    T inc = gg[j];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const T y = __shfl_up_sync(kFull, inc, o);
+                        if (lane >= o) inc = N::add(inc, y);
+                    }
+                    ex[j] = N::sub(inc, gg[j]);
+                    if (j == 0) tot0 = __shfl_sync(kFull, inc, 31);
+                }
+                ex[0] = N::add(base, ex[0]);
+                ex[1] = N::add(N::add(base, tot0), ex[1]);
+                // the cut: last candidate (in order) whose prefix is < rem
+                const bool r0 = lane < K && ex[0] < r, r1 = 32 + lane < K && ex[1] < r;
+                const unsigned m0 = __ballot_sync(kFull, r0), m1 = __ballot_sync(kFull, r1);
+                const int cx = m1 ? 32 + 31 - __clz(m1) : (m0 ? 31 - __clz(m0) : -1);
+                T add = T(0);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int x = j * 32 + lane;
+                    if (x < cx) add = N::add(add, N::mul(vv[j], gg[j]));
+                    else if (x == cx) {
+                        const T avail = N::sub(r, ex[j]);
+                        add = N::add(add, N::mul(vv[j], gg[j] < avail ? gg[j] : avail));
+                    }
+                }
+                acc = N::add(acc, add);
+            }
+        }
+        // ---- q = sum over the CTA ----
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = N::add(acc, __shfl_xor_sync(kFull, acc, o));
+        __syncthreads();
+        if (lane == 0) pb[wig] = acc;
+        __syncthreads();
+        if (t == 0) {
+            T s2 = pb[0];
+            for (int i = 1; i < NW; ++i) s2 = N::add(s2, pb[i]);
+            q[c] = s2;
+        }
+        __syncthreads();
     }
 }
 
