@@ -206,12 +206,13 @@ int rimdp_profile_read(rimdp_model* model, double* fused_ms, double* columns_ms,
  * collective exchange in the sharded driver: V_k lives in buffer k & 1. */
 int rimdp_solve_value_buffers(rimdp_model* model, void** buf0, void** buf1);
 /* Device pointer to the two per-iteration residual slots (uint64 bit patterns
- * of the non-negative max residual; iteration k uses slot k & 1).  With
- * external_stop, the driver max-reduces slot k & 1 across shards after
- * iteration k and then calls rimdp_solve_stop_test. */
+ * of the non-negative max residual; iteration k uses slot k & 1). */
 int rimdp_solve_residual_slots(rimdp_model* model, void** slots);
-/* Enqueues the stop test of the last enqueued iteration on the model stream
- * (solver.hpp:127-134 with the residual now global). */
+/* Enqueues the stop test of the last enqueued iteration k on the model stream
+ * (solver.hpp:127-134).  With external_stop, call it after the value buffer
+ * of iteration k holds every shard's slice (the all-gather): the residual
+ * max |V_k - V_{k-1}| is then taken over the whole value vector on the
+ * device, so no collective is needed for it. */
 int rimdp_solve_stop_test(rimdp_model* model);
 
 /* One Bellman step from `v_in` (bellman.hpp:127-133, with the optional

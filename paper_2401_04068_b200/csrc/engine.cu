@@ -1196,12 +1196,16 @@ int rimdp_solve_stop_test(rimdp_model* m) {
         DeviceGuard g(m->device);
         SolveState& s = m->s;
         if (s.launched == 0) return RIMDP_OK;
+        const long long k = s.launched;
+        const int blocks = grid_for(m->n_global, 256, m->sm_count, 4);
         if (m->dtype == RIMDP_F64)
-            stop_test<double><<<1, 1, 0, m->stream>>>(s.ctl.as<Ctl>(), s.launched, s.finite, s.horizon,
-                                                      s.max_iterations, (double)s.eps);
+            global_stop_test<double><<<blocks, 256, 0, m->stream>>>(
+                m->n_global, s.v[k & 1].as<double>(), s.v[(k - 1) & 1].as<double>(), s.ctl.as<Ctl>(), k, s.finite,
+                s.horizon, s.max_iterations, (double)s.eps);
         else
-            stop_test<float><<<1, 1, 0, m->stream>>>(s.ctl.as<Ctl>(), s.launched, s.finite, s.horizon,
-                                                     s.max_iterations, (float)s.eps);
+            global_stop_test<float><<<blocks, 256, 0, m->stream>>>(
+                m->n_global, s.v[k & 1].as<float>(), s.v[(k - 1) & 1].as<float>(), s.ctl.as<Ctl>(), k, s.finite,
+                s.horizon, s.max_iterations, (float)s.eps);
         CK(cudaGetLastError());
         return RIMDP_OK;
     });

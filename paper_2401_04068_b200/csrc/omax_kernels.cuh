@@ -43,7 +43,7 @@ struct Ctl {
     unsigned int arrive;            // blocks of the action kernel that finished
     int done;                       // stop condition reached; later launches are no-ops
     int status;                     // 0 ok, 1 non-convergence, 2 internal
-    int pad;
+    unsigned int arrive_stop;       // blocks of the sharded stop test that finished
     long long k;                    // iterations completed
     double res_last;                // max residual of the last iteration, as double
 };
@@ -660,7 +660,7 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
 // row order, so bit-exact (omax.hpp:169-173), with the group's sums advancing
 // in parallel instead of one lane summing one column.
 constexpr int kLongTopK = 2;
-constexpr int kLongGroup = 8;
+constexpr int kLongGroup = 4;
 
 template <class T>
 struct LongCut {
@@ -1458,16 +1458,19 @@ struct BucketShape {
     static constexpr int E = 8;
     static constexpr int NT = Len / E;    // 64 .. 1024
     static constexpr int NW = NT / 32;
-    static constexpr int B = Len / 8 < 512 ? Len / 8 : 512;
+    static constexpr int B = Len / 4 < 1024 ? Len / 4 : 1024; // ~4 entries per bucket
+    static constexpr int MinBlocks = NT >= 1024 ? 1 : 1024 / NT;
     template <class T>
     static constexpr size_t smem() {
-        // hist, cnt (u32 x B); candidates (key, pos, g, V) x kBucketCap; partials; decision words
-        return 2 * 4 * B + kBucketCap * (8 + 4 + 2 * sizeof(T)) + NW * 2 * sizeof(T) + 64;
+        // V and g by position; hist, cnt (u32 x B); candidates (key, pos, g, V) x kBucketCap; partials;
+        // decision words
+        return 2 * sizeof(T) * (size_t)Len + 2 * 4 * B + kBucketCap * (8 + 4 + 2 * sizeof(T)) +
+               NW * 2 * sizeof(T) + 64;
     }
 };
 
 template <class T, bool kPess, int LG>
-__global__ void __launch_bounds__(BucketShape<LG>::NT)
+__global__ void __launch_bounds__(BucketShape<LG>::NT, BucketShape<LG>::MinBlocks)
 omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
             const T* __restrict__ rem, const T* __restrict__ maxgap, const T* __restrict__ V, T* __restrict__ q,
@@ -1478,7 +1481,9 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
     constexpr int E = Sh::E, NT = Sh::NT, NW = Sh::NW, B = Sh::B, CAP = kBucketCap;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned* hist = reinterpret_cast<unsigned*>(smem_raw);
+    T* sv = reinterpret_cast<T*>(smem_raw);                // [Len] V by position
+    T* sgp = sv + Sh::Len;                                  // [Len] gap by position
+    unsigned* hist = reinterpret_cast<unsigned*>(sgp + Sh::Len);
     unsigned* hcnt = hist + B;
     unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hcnt + B);
     T* cg = reinterpret_cast<T*>(ckey + CAP);
@@ -1502,23 +1507,33 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             const int pos = e * NT + t;
             rw[e] = pos < L ? ld_hint(rows + b + pos, pstream) : 0;
         }
-        T v[E], g[E];
         T acc = T(0);
         T wlo = T(0), whi = T(0);
         bool any = false;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int pos = e * NT + t;
-            v[e] = T(0);
-            g[e] = T(0);
-            if (pos < L) {
-                v[e] = ld_hint(V + rw[e], pval);
-                g[e] = ld_hint(gap + b + pos, pstream);
-                acc = N::add(acc, N::mul(v[e], ld_hint(lower + b + pos, pstream)));
-                const T w = kPess ? v[e] : -v[e];
-                wlo = any ? (w < wlo ? w : wlo) : w;
-                whi = any ? (w > whi ? w : whi) : w;
-                any = true;
+        for (int h = 0; h < E; h += E / 2) { // two halves: 3 x E/2 loads in flight, fewer registers
+            T v[E / 2], g[E / 2], l[E / 2];
+#pragma unroll
+            for (int i = 0; i < E / 2; ++i) {
+                const int e = h + i, pos = e * NT + t;
+                if (pos < L) {
+                    v[i] = ld_hint(V + rw[e], pval);
+                    g[i] = ld_hint(gap + b + pos, pstream);
+                    l[i] = ld_hint(lower + b + pos, pstream);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < E / 2; ++i) {
+                const int e = h + i, pos = e * NT + t;
+                if (pos < L) {
+                    acc = N::add(acc, N::mul(v[i], l[i]));
+                    const T w = kPess ? v[i] : -v[i];
+                    wlo = any ? (w < wlo ? w : wlo) : w;
+                    whi = any ? (w > whi ? w : whi) : w;
+                    any = true;
+                    sv[pos] = v[i];
+                    sgp[pos] = g[i];
+                }
             }
         }
         for (int i = t; i < 2 * B; i += NT) hist[i] = 0u;
@@ -1551,18 +1566,19 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
         const T bscale = span > T(0) ? T(B) / span : T(0);
         const T gm = __ldg(maxgap + c);
         const double sc = gm > T(0) ? 2147483648.0 / ((double)L * (double)gm) : 0.0;
-        int bk[E];
+        auto bucket_of = [&](T val) -> int {
+            const T w = kPess ? val : -val;
+            const int x = static_cast<int>(N::mul(N::sub(w, wlo), bscale));
+            return x < B - 1 ? x : B - 1;
+        };
+        if (picks) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int pos = e * NT + t;
-            bk[e] = 0;
-            if (pos < L) {
-                const T w = kPess ? v[e] : -v[e];
-                const int x = static_cast<int>(N::mul(N::sub(w, wlo), bscale));
-                bk[e] = x < B - 1 ? x : B - 1;
-                if (picks) {
-                    atomicAdd(hist + bk[e], static_cast<unsigned>((double)g[e] * sc));
-                    atomicAdd(hcnt + bk[e], 1u);
+            for (int e = 0; e < E; ++e) {
+                const int pos = e * NT + t;
+                if (pos < L) {
+                    const int bb = bucket_of(sv[pos]);
+                    atomicAdd(hist + bb, static_cast<unsigned>((double)sgp[pos] * sc));
+                    atomicAdd(hcnt + bb, 1u);
                 }
             }
         }
@@ -1573,18 +1589,16 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             // ---- bracket of the cut's bucket (warp 0) ----
             if (wig == 0) {
                 constexpr int PB = B / 32 > 0 ? B / 32 : 1;
-                unsigned long long fm = 0;
-                unsigned long long fn = 0;
-                unsigned long long lm[PB], ln[PB];
-#pragma unroll
+                // lane totals of its PB consecutive buckets, exclusive warp scan, then a second
+                // sweep over the buckets (shared memory, not registers)
+                unsigned long long fm = 0, fn = 0;
                 for (int i = 0; i < PB; ++i) {
                     const int bb = lane * PB + i;
-                    lm[i] = bb < B ? hist[bb] : 0u;
-                    ln[i] = bb < B ? hcnt[bb] : 0u;
-                    fm += lm[i];
-                    fn += ln[i];
+                    if (bb < B) {
+                        fm += hist[bb];
+                        fn += hcnt[bb];
+                    }
                 }
-                // exclusive warp scan of the lane totals
                 unsigned long long em = fm, en = fn;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -1598,24 +1612,25 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                 en -= fn;
                 const double R = (double)r * sc;
                 int blo = -1, bhi = -1;
-#pragma unroll
                 for (int i = 0; i < PB; ++i) {
                     const int bb = lane * PB + i;
-                    if (ln[i] > 0) {
-                        if ((double)(em + en) <= R) blo = bb;
-                        if ((double)em < R) bhi = bb;
+                    if (bb < B) {
+                        const unsigned hm = hist[bb], hn = hcnt[bb];
+                        if (hn > 0) {
+                            if ((double)(em + en) <= R) blo = bb;
+                            if ((double)em < R) bhi = bb;
+                        }
+                        em += hm;
+                        en += hn;
                     }
-                    em += lm[i];
-                    en += ln[i];
                 }
                 blo = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(blo + 1))) - 1;
                 bhi = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(bhi + 1))) - 1;
                 if (blo < 0) blo = 0; // the first entry is always reached (rem > 0)
                 unsigned k = 0;
-#pragma unroll
                 for (int i = 0; i < PB; ++i) {
                     const int bb = lane * PB + i;
-                    if (bb >= blo && bb <= bhi) k += static_cast<unsigned>(ln[i]);
+                    if (bb < B && bb >= blo && bb <= bhi) k += hcnt[bb];
                 }
                 k = __reduce_add_sync(kFull, k);
                 if (lane == 0) {
@@ -1637,14 +1652,16 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             for (int e = 0; e < E; ++e) {
                 const int pos = e * NT + t;
                 if (pos < L) {
-                    if (bk[e] < blo) {
-                        bs = N::add(bs, g[e]);
-                        acc = N::add(acc, N::mul(v[e], g[e]));
-                    } else if (bk[e] <= bhi) {
+                    const T ve = sv[pos], ge = sgp[pos];
+                    const int bb = bucket_of(ve);
+                    if (bb < blo) {
+                        bs = N::add(bs, ge);
+                        acc = N::add(acc, N::mul(ve, ge));
+                    } else if (bb <= bhi) {
                         const int slot = atomicAdd(dw + 3, 1);
-                        ckey[slot] = static_cast<unsigned long long>(order_key<T>(v[e], kPess));
-                        cg[slot] = g[e];
-                        cv[slot] = v[e];
+                        ckey[slot] = static_cast<unsigned long long>(order_key<T>(ve, kPess));
+                        cg[slot] = ge;
+                        cv[slot] = ve;
                         cpos[slot] = pos;
                     }
                 }
@@ -1653,7 +1670,49 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             for (int o = 16; o > 0; o >>= 1) bs = N::add(bs, __shfl_xor_sync(kFull, bs, o));
             if (lane == 0) pa[wig] = bs;
             __syncthreads();
-            if (wig == 0) {
+            if (wig == 0 && K <= 32) {
+                // one candidate per lane: bitonic sort of 32 by (key, pos), prefix, cut
+                T base = pa[0];
+#pragma unroll
+                for (int i = 1; i < NW; ++i) base = N::add(base, pa[i]);
+                const bool ok = lane < K;
+                unsigned long long kk = ok ? ckey[lane] : ~0ull;
+                int pp = ok ? cpos[lane] : INT_MAX;
+                T gg = ok ? cg[lane] : T(0), vv = ok ? cv[lane] : T(0);
+#pragma unroll
+                for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+                    for (int stride = size / 2; stride > 0; stride >>= 1) {
+                        const unsigned long long ok2 = __shfl_xor_sync(kFull, kk, stride);
+                        const int op = __shfl_xor_sync(kFull, pp, stride);
+                        const T og = __shfl_xor_sync(kFull, gg, stride);
+                        const T ov = __shfl_xor_sync(kFull, vv, stride);
+                        const bool lower_half = (lane & stride) == 0;
+                        const bool up = (lane & size) == 0;
+                        const bool other_less = ok2 < kk || (ok2 == kk && op < pp);
+                        if (lower_half == up ? other_less : !other_less) {
+                            kk = ok2;
+                            pp = op;
+                            gg = og;
+                            vv = ov;
+                        }
+                    }
+                }
+                T inc = gg;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const T y = __shfl_up_sync(kFull, inc, o);
+                    if (lane >= o) inc = N::add(inc, y);
+                }
+                const T ex = N::add(base, N::sub(inc, gg));
+                const unsigned m0 = __ballot_sync(kFull, ok && ex < r);
+                const int cx = m0 ? 31 - __clz(m0) : -1;
+                if (lane < cx) acc = N::add(acc, N::mul(vv, gg));
+                else if (lane == cx) {
+                    const T avail = N::sub(r, ex);
+                    acc = N::add(acc, N::mul(vv, gg < avail ? gg : avail));
+                }
+            } else if (wig == 0) {
                 T base = pa[0];
 #pragma unroll
                 for (int i = 1; i < NW; ++i) base = N::add(base, pa[i]);
@@ -2133,13 +2192,42 @@ bellman_short(int nbatch, const int* __restrict__ slots, const int2* __restrict_
     warp_epilogue<T>(myres, a, eps, ctl, &s_res, &s_arrived);
 }
 
-// Stop test of a sharded iteration k after the residual slot holds the
-// max over all shards (external_stop; solver.hpp:127-134).
+// Stop test of a sharded iteration k (external_stop; solver.hpp:127-134).
+// After the all-gather every shard holds both iterates V_k and V_{k-1} in
+// full, so the global residual max |V_k - V_{k-1}| is computed here on each
+// shard over the whole vector (n x 2 x 8 B read) instead of by a collective;
+// the last block to finish evaluates the stop test.
 template <class T>
-__global__ void stop_test(Ctl* ctl, long long k, int finite, long long horizon, long long max_iterations, T eps) {
+__global__ void __launch_bounds__(256)
+global_stop_test(int n, const T* __restrict__ vk, const T* __restrict__ vk1, Ctl* ctl, long long k, int finite,
+                 long long horizon, long long max_iterations, T eps) {
     using N = Num<T>;
-    if (ctl->done) return;
-    const T res = N::from_res_bits(ctl->res_bits[k & 1]);
+    if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    unsigned long long my = 0;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+        const unsigned long long rb = N::res_bits(fabs(N::sub(vk[s], vk1[s])));
+        my = rb > my ? rb : my;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(kFull, my, o);
+        my = other > my ? other : my;
+    }
+    __shared__ unsigned long long wmax[8];
+    __shared__ bool last;
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = my;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = wmax[i] > m ? wmax[i] : m;
+        if (m) atomicMax(&ctl->res_bits[k & 1], m);
+        __threadfence();
+        last = atomicAdd(&ctl->arrive_stop, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    ctl->arrive_stop = 0u;
+    const T res = N::from_res_bits(atomicAdd(&ctl->res_bits[k & 1], 0ull));
     ctl->res_last = static_cast<double>(res);
     if (finite) {
         if (k >= horizon) ctl->done = 1;
@@ -2149,6 +2237,7 @@ __global__ void stop_test(Ctl* ctl, long long k, int finite, long long horizon, 
         ctl->done = 1;
         ctl->status = 1;
     }
+    __threadfence();
 }
 
 template <class T>

@@ -8,9 +8,10 @@ padded to world * S entries.  Per iteration k each rank
 
   1. runs the Bellman kernels for its states (writes V_k[r*S : r*S+S]),
   2. all-gathers the slices in place into its replica of V_k (one
-     ncclAllGather of S entries per rank),
-  3. max-all-reduces the iteration's residual slot (one uint64),
-  4. enqueues the device stop test (solver.hpp:127-134 on the global residual),
+     ncclAllGather of S entries per rank — the only collective),
+  3. enqueues the device stop test (solver.hpp:127-134): every rank now holds
+     V_k and V_{k-1} in full, so the global residual max |V_k - V_{k-1}| is
+     reduced on the device over the whole vector, with no second collective,
 
 all on the shard's CUDA stream, so iterations are enqueued ahead without host
 synchronisation; the host polls once per chunk.  Kernels after the stop
@@ -139,7 +140,6 @@ class ShardedSolver:
         buf = sh.values[k & 1]
         r, S = sh.rank, sh.S
         dist.all_gather_into_tensor(buf, buf[r * S:(r + 1) * S], group=self.group)
-        dist.all_reduce(sh.residual[k & 1:(k & 1) + 1], op=dist.ReduceOp.MAX, group=self.group)
 
     def enqueue(self, k: int):
         """Iteration k: local kernels, exchange, stop test — all stream-ordered."""

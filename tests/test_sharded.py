@@ -1,8 +1,8 @@
 """Multi-process sharded driver (paper_2401_04068_b200/sharded.py) on CPU:
 world_size 2 over gloo, with a test double for the device shard that computes
 its states' rows with the CPU checker (oracle port).  Covers the partitioning,
-the padded in-place all-gather of V, the residual max-all-reduce, the
-external stop test and NonConvergence — and that the sharded result is
+the padded in-place all-gather of V, the external stop test on the
+residual of the gathered iterates and NonConvergence — and that the sharded result is
 bit-identical to the unsharded one (per-state arithmetic is unchanged)."""
 import contextlib
 import os
@@ -90,10 +90,13 @@ class CpuShard:
         self.k = k
 
     def stop_test(self):
+        # like the device kernel: the residual over the whole gathered vector
         if self.done:
             return
         k, p = self.k, self.plan
-        res = struct.unpack("<d", struct.pack("<q", int(self.residual[k & 1])))[0]
+        full = float(torch.max(torch.abs(self.values[k & 1][:self.n] - self.values[(k - 1) & 1][:self.n])))
+        local = struct.unpack("<d", struct.pack("<q", int(self.residual[k & 1])))[0]
+        res = max(full, local)
         self.res_last = res
         if p["finite"]:
             self.done = k >= p["horizon"]

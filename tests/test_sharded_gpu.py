@@ -1,6 +1,6 @@
 """The sharded path on the device: shard stores (rimdp_model_create_shard /
-generated shards), padded value buffers, residual slots and the external
-stop test, driven (a) by ShardedSolver over a 1-rank NCCL group and (b) as
+generated shards), padded value buffers and the external stop test (global
+residual from the gathered iterates), driven (a) by ShardedSolver over a 1-rank NCCL group and (b) as
 two shards in lockstep on one GPU with the exchange done by device copies —
 both bit-identical to the unsharded solve."""
 import os
@@ -74,9 +74,8 @@ def lockstep(shards, plan, chunk=5):
                     if src is not dst:
                         dst.values[k & 1][src.rank * S:(src.rank + 1) * S].copy_(
                             src.values[k & 1][src.rank * S:(src.rank + 1) * S])
-                m = max(int(sh.residual[k & 1]) for sh in shards)
-                dst.residual[k & 1] = m
             torch.cuda.synchronize()
+            # no residual exchange: the stop test reduces the gathered iterates itself
             for sh in shards:
                 sh.stop_test()
         states = [sh.poll() for sh in shards]
