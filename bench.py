@@ -45,7 +45,7 @@ WORKLOADS = {
                     "Pmaxmin InfiniteTimeReachability(goal = last 1% of states, eps = 1e-6)",
                source="reference", states=100000, actions=4, density=32.0 / 100000, scale=1.0 / 32, seed=1,
                kind="reach", goal_frac=0.01, pessimistic=True, maximize=True, eps=1e-6,
-               sample=None),
+               sample=None, weak_support=32),
     "c3": dict(desc="C3: random_imdp 2000 states x 10 actions x 2000 successors (40M transitions), "
                     "Pminmin InfiniteTimeReachability(goal = last 1%, eps = 1e-6), long-column path",
                source="reference", states=2000, actions=10, density=1.0, scale=1.0 / 2000, seed=1,
@@ -66,6 +66,22 @@ WORKLOADS = {
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def scaled_workload(w, world, scaling):
+    """The workload at `world` GPUs.  Weak scaling (the default for C2, the
+    default config): the same law with world x the states, so every GPU
+    keeps C2's 100000 states x 4 actions x 32 successors (density 32 / n).
+    Configs 3-5 are fixed-size (C4 is already the 8-GPU shard config):
+    strong scaling."""
+    if scaling == "weak" and world > 1 and w.get("weak_support"):
+        n = w["states"] * world
+        w = dict(w, states=n, density=w["weak_support"] / n,
+                 desc=w["desc"].split(":")[0] + f" weak-scaled x{world}: random_imdp {n} states x {w['actions']} "
+                      f"actions x {w['weak_support']} successors, Pmaxmin InfiniteTimeReachability(goal = last 1%, "
+                      "eps = 1e-6)")
+        return w, "weak"
+    return w, ("weak" if (w.get("weak_support") and scaling == "weak") else "strong")
 
 
 def load_peaks():
@@ -344,7 +360,7 @@ def engine_arm(args, w):
     d2h = values.nbytes + residual.nbytes
     ref_iters = bit_exact = None
     gj = os.path.join(ROOT, "tests", "golden", f"{args.config}.json")
-    if os.path.exists(gj) and args.dtype == "f64":
+    if os.path.exists(gj) and args.dtype == "f64" and w["states"] == WORKLOADS[args.config]["states"]:
         import hashlib
         with open(gj) as f:
             run = json.load(f)["runs"].get(f"m{int(w['maximize'])}p{int(w['pessimistic'])}")
@@ -367,7 +383,7 @@ def engine_arm(args, w):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling_kind,
         "vs_baseline": None,
         "dtype": args.dtype,
         "data": ("synthetic (reference random_imdp law, seed 1; generated on host, resident in HBM)"
@@ -400,7 +416,6 @@ def engine_arm(args, w):
     }
     if world > 1:
         out["config"]["shard_nnz_max_over_mean"] = max_nnz / (total_nnz / world)
-        out["scaling"] = "strong"
     if cpu:
         out["cpu_baseline"] = cpu
     if rank == 0:
@@ -477,7 +492,7 @@ def reference_arm(args, w):
     out = {"impl": "reference", "metric": "transitions/sec per Bellman iteration", "value": v,
            "unit": "transitions/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": (nnz_full / v * 1e3) if nnz_full else None,
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+           "higher_is_better": True, "scaling": args.scaling_kind, "vs_baseline": None, "dtype": args.dtype,
            "data": "synthetic (same generator and seed as the engine arm)",
            "config": {"workload": w["desc"], "states": w["states"], "transitions": nnz_full,
                       "parallelism": f"host threads ({os.cpu_count()})"},
@@ -496,10 +511,13 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak (C2 law, N x the states) or strong (fixed model)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    w = WORKLOADS[args.config]
+    w, args.scaling_kind = scaled_workload(WORKLOADS[args.config], int(os.environ.get("WORLD_SIZE", "1")),
+                                           args.scaling)
     if args.impl == "reference":
         reference_arm(args, w)
     else:

@@ -399,11 +399,14 @@ void init_common(rimdp_model* m, int device) {
 // and every V[row] gather costs a 32-byte DRAM sector.  An access-policy
 // window marks the buffer the iteration reads as persisting in a set-aside
 // part of L2 (cudaLimitPersistingL2CacheSize); the window follows the double
-// buffer from iteration to iteration.  RIMDP_L2_PERSIST=0 disables it.
+// buffer from iteration to iteration.  Opt-in (RIMDP_L2_PERSIST=1): on
+// config 4 it cuts DRAM reads from 188 to 110 GB per iteration but the
+// kernel gets slower (45 vs 38 ms: profiles/round1/ncu_c4_omax_medium_*),
+// so the default relies on the per-load evict-first / evict-last hints.
 void setup_l2_persistence(rimdp_model* m, size_t value_bytes) {
     m->l2_persist = 0;
     const char* e = getenv("RIMDP_L2_PERSIST");
-    if (e && atoi(e) == 0) return;
+    if (!e || atoi(e) == 0) return;
     if (value_bytes < (8u << 20)) return; // small V stays in L2 anyway
     int max_persist = 0;
     if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, m->device) != cudaSuccess ||

@@ -459,7 +459,7 @@ struct MediumShape {
 };
 
 template <class T, bool kPess, int E>
-__global__ void __launch_bounds__(MediumShape<E>::W * 32)
+__global__ void __launch_bounds__(MediumShape<E>::W * 32, E == 2 ? 4 : 2)
 omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
             const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl,
@@ -685,7 +685,8 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
     using Bits = typename N::Bits;
     constexpr int K = kLongTopK, U = 4, G = kLongGroup;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
-    __shared__ T xs[kWarpsPerBlock][G][33];
+    constexpr int UB = 2; // phase B: chunks per round
+    __shared__ T xs[kWarpsPerBlock][G][32 * UB + 1];
     __shared__ LongCut<T> cuts[kWarpsPerBlock][G];
     extern __shared__ __align__(16) unsigned char vs_raw[];
     const T* __restrict__ V = Vg;
@@ -861,38 +862,49 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
         // ---- phase B: row-order expectations of the group, chunk by chunk ----
         const int maxL = __reduce_max_sync(kFull, static_cast<unsigned>(mlen));
         T acc = T(0);
-        for (int j0 = 0; j0 < maxL; j0 += 32) {
-            const int j = j0 + lane;
-            int rw[G];
+        for (int j0 = 0; j0 < maxL; j0 += 32 * UB) {
+            // loads of G x UB chunks in flight: rows first, then (V, lower) of each
+            int rw[G][UB];
+            T lw[G][UB];
 #pragma unroll
             for (int jc = 0; jc < G; ++jc) {
                 const long long b = __shfl_sync(kFull, mbeg, jc);
                 const int L = __shfl_sync(kFull, mlen, jc);
-                rw[jc] = (jc < ng && j < L) ? __ldg(rows + b + j) : 0;
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int j = j0 + u * 32 + lane;
+                    const bool ok = jc < ng && j < L;
+                    rw[jc][u] = ok ? __ldg(rows + b + j) : 0;
+                    lw[jc][u] = ok ? __ldg(lower + b + j) : T(0);
+                }
             }
 #pragma unroll
             for (int jc = 0; jc < G; ++jc) {
                 const long long b = __shfl_sync(kFull, mbeg, jc);
                 const int L = __shfl_sync(kFull, mlen, jc);
-                if (jc < ng && j < L) {
-                    const T v = V[rw[jc]];
-                    const T l = __ldg(lower + b + j);
-                    const LongCut<T>& cu = cuts[w][jc];
-                    T p = l;
-                    if (cu.lastp >= 0) {
-                        const Bits k = N::key(v, kPess);
-                        if (k < cu.lastk || (k == cu.lastk && j <= cu.lastp)) {
-                            p = N::add(l, __ldg(gap + b + j));
-                            for (int t = 0; t < cu.npart; ++t)
-                                if (cu.ppos[t] == j) p = cu.pval[t];
+                const LongCut<T>& cu = cuts[w][jc];
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                    const int j = j0 + u * 32 + lane;
+                    if (jc < ng && j < L) {
+                        const T v = V[rw[jc][u]];
+                        const T l = lw[jc][u];
+                        T p = l;
+                        if (cu.lastp >= 0) {
+                            const Bits k = N::key(v, kPess);
+                            if (k < cu.lastk || (k == cu.lastk && j <= cu.lastp)) {
+                                p = N::add(l, __ldg(gap + b + j));
+                                for (int t = 0; t < cu.npart; ++t)
+                                    if (cu.ppos[t] == j) p = cu.pval[t];
+                            }
                         }
+                        xs[w][jc][u * 32 + lane] = N::mul(v, p);
                     }
-                    xs[w][jc][lane] = N::mul(v, p);
                 }
             }
             __syncwarp();
             if (lane < ng) {
-                const int m = min(32, mlen - j0);
+                const int m = min(32 * UB, mlen - j0);
                 for (int t = 0; t < m; ++t) acc = N::add(acc, xs[w][lane][t]);
             }
             __syncwarp();

@@ -30,3 +30,20 @@ def test_random_imdp_f32_matches_reference_generator(golden):
     got = engine.random_imdp(60, 3, 0.2, 1.0 / 12, 9, dtype=np.float32)
     for g, e in zip(got, golden.model("f32r60")):
         assert np.array_equal(np.asarray(g), np.asarray(e))
+
+
+def test_bench_weak_scaling_keeps_per_gpu_work():
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    c2 = bench.WORKLOADS["c2"]
+    w1, k1 = bench.scaled_workload(c2, 1, "weak")
+    w8, k8 = bench.scaled_workload(c2, 8, "weak")
+    assert w1 is c2 and k1 == "weak" and k8 == "weak"
+    assert w8["states"] == 8 * c2["states"] and abs(w8["density"] * w8["states"] - 32) < 1e-9
+    w4, k4 = bench.scaled_workload(bench.WORKLOADS["c4"], 4, "weak")
+    assert w4["states"] == bench.WORKLOADS["c4"]["states"] and k4 == "strong"
+    ws, ks = bench.scaled_workload(c2, 8, "strong")
+    assert ws is c2 and ks == "strong"
