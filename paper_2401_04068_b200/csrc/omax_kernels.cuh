@@ -459,7 +459,7 @@ struct MediumShape {
 };
 
 template <class T, bool kPess, int E>
-__global__ void __launch_bounds__(MediumShape<E>::W * 32, E == 2 ? 4 : 2)
+__global__ void __launch_bounds__(MediumShape<E>::W * 32)
 omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
             const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl,
