@@ -1,0 +1,346 @@
+// Native IMDPCSC1 model containers -> the engine's CSC arrays (SURVEY §8f
+// rank 2): the on-disk form of the device store, read without building the
+// reference's host objects, then uploaded with rimdp_model_create and checked
+// on the device (rimdp_model_validate).
+//
+// Follows read_native_model (io/native.hpp:457-561):
+//   * container: magic "IMDPCSC1", u32 attribute count, (u32 len, key, u32
+//     len, value)*, u32 variable count, (u32 len, key, u8 dtype, u64 count,
+//     payload)* with dtype 1 int32, 2 f64, 3 f32, 4 string, 5 rational
+//     (native.hpp:15-41, 295-347);
+//   * attributes model = imc|imdp, format = sparse_csc, rows = to,
+//     cols = from | from/action, num_states > 0 (native.hpp:486-500);
+//   * variables lower/upper colptr/rowval (int32) and nzval (f64 or f32: an
+//     f64 store accepts either, an f32 store only f32 — NativeValueCodec,
+//     native.hpp:206-225); stateptr + action_vals for imdp; imc promotes to
+//     one action "0" per state (native.hpp:519-532);
+//   * row bounds (native.hpp:536-541), CscMatrix::structural_violation of
+//     both matrices (csc.hpp:75-107), the pattern merge of
+//     IntervalProbabilities::align (interval.hpp:218-252) and the removal of
+//     [0, 0] entries (interval.hpp:261-279);
+//   * IntervalMDP::validate's structure checks (imdp.hpp:129-168).
+// Entry and column-sum checks (interval.hpp:132-179) run on the device at
+// upload (rimdp_model_validate).  Every failure is a SchemaViolation whose
+// message is "<path>: <reason>" as in the reference.
+#include "rimdp_b200.h"
+
+#include <charconv>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+extern "C" int rimdp_internal_fail(int status, const char* msg);
+
+namespace {
+
+struct SchemaError : std::runtime_error {
+    int status;
+    SchemaError(int st, const std::string& m) : std::runtime_error(m), status(st) {}
+};
+
+struct Var {
+    uint8_t dtype = 0;
+    std::vector<int32_t> i32;
+    std::vector<double> f64;
+    std::vector<float> f32;
+    std::vector<std::string> str;
+    uint64_t count = 0;
+};
+
+class Reader {
+public:
+    Reader(const std::string& path) : path_(path), in_(path, std::ios::binary) {
+        if (!in_) throw SchemaError(RIMDP_ERR_MISSING_FILE, "missing file: " + path); // errors.hpp MissingFile
+    }
+    // SchemaViolation (errors.hpp:92-95) thrown as path + ": " + reason (native.hpp:459-461)
+    [[noreturn]] void fail(const std::string& why) {
+        throw SchemaError(RIMDP_ERR_SCHEMA, "schema violation: " + path_ + ": " + why);
+    }
+    // a ModelError caught by read_native_model (native.hpp:557-559): Violation::to_string (errors.hpp:156-163)
+    [[noreturn]] void model_error(const char* kind, const std::string& msg, long long state = -1,
+                                  long long column = -1, long long row = -1) {
+        std::string v = kind;
+        if (state >= 0) v += " state=" + std::to_string(state);
+        if (column >= 0) v += " column=" + std::to_string(column);
+        if (row >= 0) v += " row=" + std::to_string(row);
+        fail(v + ": " + msg);
+    }
+    void bytes(void* p, size_t n) {
+        in_.read(static_cast<char*>(p), static_cast<std::streamsize>(n));
+        if (static_cast<size_t>(in_.gcount()) != n) fail("truncated file");
+    }
+    uint8_t u8() { uint8_t v; bytes(&v, 1); return v; }
+    uint32_t u32() { uint32_t v; bytes(&v, 4); return v; }
+    uint64_t u64() { uint64_t v; bytes(&v, 8); return v; }
+    std::string str() {
+        const uint32_t n = u32();
+        if (n > (1u << 30)) fail("string length implausibly large");
+        std::string s(n, '\0');
+        if (n) bytes(s.data(), n);
+        return s;
+    }
+
+private:
+    std::string path_;
+    std::ifstream in_;
+};
+
+template <class V>
+struct Model {
+    int32_t num_states = 0;
+    int32_t num_cols = 0;
+    bool imdp = true;
+    std::vector<int32_t> stateptr;
+    std::vector<int64_t> colptr;
+    std::vector<int32_t> rowval;
+    std::vector<V> lower, upper;
+    std::vector<std::string> labels;
+};
+
+template <class V>
+std::unique_ptr<Model<V>> read_model(const std::string& path) {
+    Reader in(path);
+    char magic[8];
+    {
+        std::ifstream probe(path, std::ios::binary);
+        probe.read(magic, 8);
+        if (probe.gcount() != 8 || std::memcmp(magic, "IMDPCSC1", 8) != 0)
+            in.fail("not an IMDPCSC1 binary container (the JSON debug variant is read by the reference "
+                    "tools only)");
+    }
+    in.bytes(magic, 8);
+    std::map<std::string, std::string> attrs;
+    std::map<std::string, Var> vars;
+    const uint32_t na = in.u32();
+    for (uint32_t i = 0; i < na; ++i) {
+        std::string k = in.str();
+        attrs[k] = in.str();
+    }
+    const uint32_t nv = in.u32();
+    for (uint32_t i = 0; i < nv; ++i) {
+        std::string key = in.str();
+        Var v;
+        v.dtype = in.u8();
+        v.count = in.u64();
+        if (v.count > (1ull << 33)) in.fail("variable " + key + " implausibly large");
+        switch (v.dtype) {
+        case 1: v.i32.resize(v.count); if (v.count) in.bytes(v.i32.data(), 4 * v.count); break;
+        case 2: v.f64.resize(v.count); if (v.count) in.bytes(v.f64.data(), 8 * v.count); break;
+        case 3: v.f32.resize(v.count); if (v.count) in.bytes(v.f32.data(), 4 * v.count); break;
+        case 4: v.str.resize(v.count); for (auto& s : v.str) s = in.str(); break;
+        case 5: {
+            std::vector<int64_t> skip(2 * v.count);
+            if (v.count) in.bytes(skip.data(), 16 * v.count);
+            break;
+        }
+        default: in.fail("unknown dtype " + std::to_string(v.dtype) + " for variable " + key);
+        }
+        vars[key] = std::move(v);
+    }
+    auto attr = [&](const char* k) -> const std::string& {
+        auto it = attrs.find(k);
+        if (it == attrs.end()) in.fail(std::string("missing attribute ") + k);
+        return it->second;
+    };
+    const std::string model = attr("model");
+    if (model != "imc" && model != "imdp") in.fail("model must be imc or imdp");
+    if (attr("format") != "sparse_csc") in.fail("format must be sparse_csc");
+    if (attr("rows") != "to") in.fail("rows must be to");
+    const std::string expected_cols = model == "imc" ? "from" : "from/action";
+    if (attr("cols") != expected_cols) in.fail("cols must be " + expected_cols + " for model " + model);
+    long long ns = -1;
+    {
+        const std::string& s = attr("num_states");
+        auto r = std::from_chars(s.data(), s.data() + s.size(), ns);
+        if (r.ec != std::errc() || r.ptr != s.data() + s.size()) ns = -1;
+    }
+    if (ns <= 0 || ns > INT32_MAX) in.fail("bad num_states");
+    auto var = [&](const char* k) -> Var& {
+        auto it = vars.find(k);
+        if (it == vars.end()) in.fail(std::string("missing variable ") + k);
+        return it->second;
+    };
+    auto ints = [&](const char* k) -> std::vector<int32_t>& {
+        Var& v = var(k);
+        if (v.dtype != 1) in.fail(std::string("variable ") + k + " must be int32");
+        return v.i32;
+    };
+    auto values = [&](const char* k) -> std::vector<V> {
+        Var& v = var(k);
+        std::vector<V> out;
+        if constexpr (sizeof(V) == 8) {
+            if (v.dtype == 2) out.assign(v.f64.begin(), v.f64.end());
+            else if (v.dtype == 3) out.assign(v.f32.begin(), v.f32.end());
+            else in.fail(std::string("variable ") + k + " is not floating point");
+        } else {
+            if (v.dtype != 3) in.fail(std::string("variable ") + k + " is not float32; convert explicitly");
+            out.assign(v.f32.begin(), v.f32.end());
+        }
+        return out;
+    };
+    const std::vector<int32_t>& lcp = ints("lower_colptr");
+    const std::vector<int32_t>& lrv = ints("lower_rowval");
+    const std::vector<int32_t>& ucp = ints("upper_colptr");
+    const std::vector<int32_t>& urv = ints("upper_rowval");
+    const std::vector<V> lnz = values("lower_nzval");
+    const std::vector<V> unz = values("upper_nzval");
+    if (ucp.empty()) in.fail("empty upper_colptr");
+    const int64_t ncols = static_cast<int64_t>(ucp.size()) - 1;
+    if (static_cast<int64_t>(lcp.size()) - 1 != ncols) in.fail("lower and upper matrices must have the same column count");
+
+    auto m = std::make_unique<Model<V>>();
+    m->num_states = static_cast<int32_t>(ns);
+    m->num_cols = static_cast<int32_t>(ncols);
+    m->imdp = model == "imdp";
+    if (m->imdp) {
+        m->stateptr = ints("stateptr");
+        Var& lab = var("action_vals");
+        if (lab.dtype != 4) in.fail("variable action_vals must be strings");
+        m->labels = std::move(lab.str);
+    } else {
+        if (ncols != ns) in.fail("imc requires one column per state");
+        m->stateptr.resize(ns + 1);
+        for (int32_t s = 0; s <= ns; ++s) m->stateptr[s] = s;
+        m->labels.assign(ns, "0");
+    }
+    for (int32_t r : lrv)
+        if (r < 0 || r >= ns) in.fail("IndexOutOfBounds: lower_rowval entry");
+    for (int32_t r : urv)
+        if (r < 0 || r >= ns) in.fail("IndexOutOfBounds: upper_rowval entry");
+    // CscMatrix::from_csc -> structural_violation (csc.hpp:75-107); ModelError -> SchemaViolation
+    auto structural = [&](const std::vector<int32_t>& cp, const std::vector<int32_t>& rv, size_t nz) {
+        const char* SE = "StructuralError";
+        if (cp.front() != 0) in.model_error(SE, "colptr must start at 0");
+        if (cp.back() != static_cast<int64_t>(rv.size()) || rv.size() != nz)
+            in.model_error(SE, "value arrays do not match colptr");
+        for (int64_t j = 0; j < ncols; ++j) {
+            if (cp[j] > cp[j + 1]) in.model_error(SE, "colptr not monotone", -1, j);
+            for (int64_t k = cp[j]; k < cp[j + 1]; ++k)
+                if (k > cp[j] && rv[k] <= rv[k - 1])
+                    in.model_error(SE, "row indices not strictly increasing within column", -1, j, rv[k]);
+        }
+    };
+    structural(lcp, lrv, lnz.size());
+    structural(ucp, urv, unz.size());
+    // align (interval.hpp:218-252), then drop [0, 0] entries (:261-279)
+    m->colptr.reserve(ncols + 1);
+    m->colptr.push_back(0);
+    m->rowval.reserve(urv.size());
+    m->lower.reserve(urv.size());
+    m->upper.reserve(urv.size());
+    for (int64_t j = 0; j < ncols; ++j) {
+        int64_t a = lcp[j], ae = lcp[j + 1], b = ucp[j], be = ucp[j + 1];
+        while (a < ae || b < be) {
+            const int32_t ra = a < ae ? lrv[a] : INT32_MAX, rb = b < be ? urv[b] : INT32_MAX;
+            int32_t r;
+            V lo, up;
+            if (ra < rb) { r = ra; lo = lnz[a++]; up = V(0); }
+            else if (rb < ra) { r = rb; lo = V(0); up = unz[b++]; }
+            else { r = ra; lo = lnz[a++]; up = unz[b++]; }
+            if (lo == V(0) && up == V(0)) continue;
+            m->rowval.push_back(r);
+            m->lower.push_back(lo);
+            m->upper.push_back(up);
+        }
+        m->colptr.push_back(static_cast<int64_t>(m->rowval.size()));
+    }
+    // IntervalMDP structure (imdp.hpp:129-168): the first violation of the report
+    const auto& sp = m->stateptr;
+    const char* SE = "StructuralError";
+    if (sp.empty() || sp.front() != 0) in.model_error(SE, "stateptr must start at 0");
+    const int64_t nst = static_cast<int64_t>(sp.size()) - 1;
+    if (nst != ns)
+        in.model_error("DestinationCountMismatch", "transition matrix has " + std::to_string(ns) +
+                                                       " destinations for " + std::to_string(nst) + " states");
+    if (sp.back() != ncols)
+        in.model_error(SE, "stateptr must end at the column count (" + std::to_string(sp.back()) + " != " +
+                               std::to_string(ncols) + ")");
+    if (static_cast<int64_t>(m->labels.size()) != ncols) in.model_error(SE, "one action label required per column");
+    for (int64_t s = 0; s < nst; ++s) {
+        if (sp[s + 1] <= sp[s]) in.model_error("EmptyActionSet", "state has no actions", s);
+        std::unordered_set<std::string> seen;
+        for (int32_t c = sp[s]; c < sp[s + 1]; ++c)
+            if (!seen.insert(m->labels[c]).second)
+                in.model_error("DuplicateActionLabel", "action \"" + m->labels[c] + "\" occurs twice", s, c);
+    }
+    return m;
+}
+
+struct Handle {
+    int dtype;
+    std::unique_ptr<Model<double>> d;
+    std::unique_ptr<Model<float>> f;
+};
+
+template <class V>
+void sizes_of(const Model<V>& m, rimdp_native_sizes* s) {
+    s->num_states = m.num_states;
+    s->num_cols = m.num_cols;
+    s->nnz = static_cast<int64_t>(m.rowval.size());
+    s->imdp = m.imdp;
+    int64_t lb = 0;
+    for (const auto& l : m.labels) lb += static_cast<int64_t>(l.size()) + 1;
+    s->label_bytes = lb;
+}
+
+template <class V>
+void take(const Model<V>& m, int32_t* sp, int64_t* cp, int32_t* rv, void* lo, void* up, char* labels) {
+    if (sp) std::memcpy(sp, m.stateptr.data(), sizeof(int32_t) * m.stateptr.size());
+    if (cp) std::memcpy(cp, m.colptr.data(), sizeof(int64_t) * m.colptr.size());
+    if (rv) std::memcpy(rv, m.rowval.data(), sizeof(int32_t) * m.rowval.size());
+    if (lo) std::memcpy(lo, m.lower.data(), sizeof(V) * m.lower.size());
+    if (up) std::memcpy(up, m.upper.data(), sizeof(V) * m.upper.size());
+    if (labels)
+        for (const auto& l : m.labels) {
+            std::memcpy(labels, l.c_str(), l.size() + 1);
+            labels += l.size() + 1;
+        }
+}
+
+} // namespace
+
+extern "C" {
+
+int rimdp_native_read(const char* path, int32_t dtype, rimdp_native_sizes* sizes, void** handle) {
+    if (!path || !sizes || !handle || (dtype != RIMDP_F64 && dtype != RIMDP_F32))
+        return rimdp_internal_fail(RIMDP_ERR_INVALID_ARGUMENT, "rimdp_native_read: bad argument");
+    try {
+        auto h = std::make_unique<Handle>();
+        h->dtype = dtype;
+        if (dtype == RIMDP_F64) {
+            h->d = read_model<double>(path);
+            sizes_of(*h->d, sizes);
+        } else {
+            h->f = read_model<float>(path);
+            sizes_of(*h->f, sizes);
+        }
+        *handle = h.release();
+        return RIMDP_OK;
+    } catch (const SchemaError& e) {
+        return rimdp_internal_fail(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return rimdp_internal_fail(RIMDP_ERR_OUT_OF_MEMORY, "host allocation failed");
+    }
+}
+
+int rimdp_native_take(void* handle, int32_t* stateptr, int64_t* colptr, int32_t* rowval, void* lower, void* upper,
+                      char* labels) {
+    if (!handle) return rimdp_internal_fail(RIMDP_ERR_INVALID_ARGUMENT, "rimdp_native_take: null handle");
+    Handle* h = static_cast<Handle*>(handle);
+    if (h->dtype == RIMDP_F64)
+        take(*h->d, stateptr, colptr, rowval, lower, upper, labels);
+    else
+        take(*h->f, stateptr, colptr, rowval, lower, upper, labels);
+    return RIMDP_OK;
+}
+
+void rimdp_native_free(void* handle) { delete static_cast<Handle*>(handle); }
+
+} // extern "C"

@@ -1477,7 +1477,7 @@ struct BucketShape {
         // V and g by position; hist, cnt (u32 x B); candidates (key, pos, g, V) x kBucketCap; partials;
         // decision words
         return 2 * sizeof(T) * (size_t)Len + 2 * 4 * B + kBucketCap * (8 + 4 + 2 * sizeof(T)) +
-               NW * 2 * sizeof(T) + 64;
+               NW * (2 * sizeof(T) + 16) + 64;
     }
 };
 
@@ -1503,7 +1503,8 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
     int* cpos = reinterpret_cast<int*>(cv + CAP);
     T* pa = reinterpret_cast<T*>(cpos + CAP);   // [NW] partial A
     T* pb = pa + NW;                            // [NW] partial B
-    int* dw = reinterpret_cast<int*>(pb + NW);   // decision: b_lo, b_hi, K, ncand counter
+    unsigned long long* wtot = reinterpret_cast<unsigned long long*>(pb + NW); // [2][NW] warp scan totals
+    int* dw = reinterpret_cast<int*>(wtot + 2 * NW); // b_lo + 1, b_hi + 1, -, candidate counter
     const int t = threadIdx.x, lane = t & 31, wig = t >> 5;
     const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
 
@@ -1549,7 +1550,7 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             }
         }
         for (int i = t; i < 2 * B; i += NT) hist[i] = 0u;
-        if (t == 0) dw[3] = 0;
+        if (t < 4) dw[t] = 0;
         if (!any) { // only threads past the end of a short column
             wlo = T(1e300);
             whi = T(-1e300);
@@ -1598,34 +1599,43 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
         if (!picks) {
             // no picks: q = sum V l
         } else {
-            // ---- bracket of the cut's bucket (warp 0) ----
-            if (wig == 0) {
-                constexpr int PB = B / 32 > 0 ? B / 32 : 1;
-                // lane totals of its PB consecutive buckets, exclusive warp scan, then a second
-                // sweep over the buckets (shared memory, not registers)
-                unsigned long long fm = 0, fn = 0;
-                for (int i = 0; i < PB; ++i) {
-                    const int bb = lane * PB + i;
-                    if (bb < B) {
-                        fm += hist[bb];
-                        fn += hcnt[bb];
-                    }
-                }
-                unsigned long long em = fm, en = fn;
+            // ---- bracket of the cut's bucket: block-wide exclusive scan of the buckets ----
+            constexpr int PB = B / NT > 0 ? B / NT : 1; // buckets per thread
+            unsigned long long fm = 0, fn = 0;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned long long a = __shfl_up_sync(kFull, em, o), z = __shfl_up_sync(kFull, en, o);
-                    if (lane >= o) {
-                        em += a;
-                        en += z;
-                    }
+            for (int i = 0; i < PB; ++i) {
+                const int bb = t * PB + i;
+                if (bb < B) {
+                    fm += hist[bb];
+                    fn += hcnt[bb];
                 }
-                em -= fm;
-                en -= fn;
+            }
+            unsigned long long em = fm, en = fn;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long a = __shfl_up_sync(kFull, em, o), z = __shfl_up_sync(kFull, en, o);
+                if (lane >= o) {
+                    em += a;
+                    en += z;
+                }
+            }
+            if (lane == 31) {
+                wtot[wig] = em;
+                wtot[NW + wig] = en;
+            }
+            __syncthreads();
+            em -= fm;
+            en -= fn;
+            for (int i = 0; i < wig; ++i) {
+                em += wtot[i];
+                en += wtot[NW + i];
+            }
+            {
                 const double R = (double)r * sc;
                 int blo = -1, bhi = -1;
+#pragma unroll
                 for (int i = 0; i < PB; ++i) {
-                    const int bb = lane * PB + i;
+                    const int bb = t * PB + i;
                     if (bb < B) {
                         const unsigned hm = hist[bb], hn = hcnt[bb];
                         if (hn > 0) {
@@ -1636,28 +1646,12 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                         en += hn;
                     }
                 }
-                blo = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(blo + 1))) - 1;
-                bhi = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(bhi + 1))) - 1;
-                if (blo < 0) blo = 0; // the first entry is always reached (rem > 0)
-                unsigned k = 0;
-                for (int i = 0; i < PB; ++i) {
-                    const int bb = lane * PB + i;
-                    if (bb < B && bb >= blo && bb <= bhi) k += hcnt[bb];
-                }
-                k = __reduce_add_sync(kFull, k);
-                if (lane == 0) {
-                    dw[0] = blo;
-                    dw[1] = bhi;
-                    dw[2] = static_cast<int>(k);
-                }
+                if (blo >= 0) atomicMax(dw + 0, blo + 1);
+                if (bhi >= 0) atomicMax(dw + 1, bhi + 1);
             }
             __syncthreads();
-            const int blo = dw[0], bhi = dw[1], K = dw[2];
-            if (K > CAP) {
-                if (t == 0) fallback[atomicAdd(nfallback, 1)] = c;
-                __syncthreads(); // keep dw / hist stable until everyone has read them
-                continue;
-            }
+            const int blo = dw[0] > 0 ? dw[0] - 1 : 0; // the first entry is always reached (rem > 0)
+            const int bhi = dw[1] - 1;
             // ---- entries before the bracket; candidates to shared memory ----
             T bs = T(0);
 #pragma unroll
@@ -1671,10 +1665,12 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                         acc = N::add(acc, N::mul(ve, ge));
                     } else if (bb <= bhi) {
                         const int slot = atomicAdd(dw + 3, 1);
-                        ckey[slot] = static_cast<unsigned long long>(order_key<T>(ve, kPess));
-                        cg[slot] = ge;
-                        cv[slot] = ve;
-                        cpos[slot] = pos;
+                        if (slot < CAP) {
+                            ckey[slot] = static_cast<unsigned long long>(order_key<T>(ve, kPess));
+                            cg[slot] = ge;
+                            cv[slot] = ve;
+                            cpos[slot] = pos;
+                        }
                     }
                 }
             }
@@ -1682,6 +1678,13 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             for (int o = 16; o > 0; o >>= 1) bs = N::add(bs, __shfl_xor_sync(kFull, bs, o));
             if (lane == 0) pa[wig] = bs;
             __syncthreads();
+            const int K = dw[3];
+            if (K > CAP) {
+                // too many entries in the bracket (ties, clustered values): selection kernel
+                if (t == 0) fallback[atomicAdd(nfallback, 1)] = c;
+                __syncthreads(); // dw / hist / candidates stay stable until everyone has read them
+                continue;
+            }
             if (wig == 0 && K <= 32) {
                 // one candidate per lane: bitonic sort of 32 by (key, pos), prefix, cut
                 T base = pa[0];
