@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define RIMDP_B200_ABI_VERSION 2
+#define RIMDP_B200_ABI_VERSION 3
 
 /* Scalar type of a model: NumericTraits<double|float> (numeric.hpp:53-81).
  * The exact Rational instantiation (numeric.hpp:83-101) has no device path. */
@@ -43,7 +43,9 @@ typedef enum rimdp_status {
     RIMDP_ERR_CUDA = 4,
     RIMDP_ERR_OUT_OF_MEMORY = 5,
     RIMDP_ERR_NO_DEVICE = 6,
-    RIMDP_ERR_INTERNAL = 7
+    RIMDP_ERR_INTERNAL = 7,
+    RIMDP_ERR_MISSING_FILE = 8,      /* io::MissingFile (errors.hpp), native model containers */
+    RIMDP_ERR_SCHEMA = 9             /* io::SchemaViolation (errors.hpp:92-95), native.hpp:459-461 */
 } rimdp_status;
 
 typedef struct rimdp_model rimdp_model; /* opaque, owns the device CSC store */
@@ -146,6 +148,30 @@ typedef struct rimdp_model_info {
 int rimdp_model_info_get(rimdp_model* model, rimdp_model_info* out);
 /* The CUDA stream (cudaStream_t) every kernel of this model is launched on. */
 int rimdp_model_stream(rimdp_model* model, void** stream_out);
+
+/* ---- native IMDPCSC1 containers --------------------
+ * Replaces io::read_native_model (io/native.hpp:457-561) for the engine:
+ * the container's named CSC arrays (native.hpp:15-41) are read, checked
+ * (attributes, CscMatrix structure csc.hpp:75-107, the pattern merge of
+ * IntervalProbabilities::align interval.hpp:218-252, [0,0] removal :261-279,
+ * IntervalMDP structure imdp.hpp:129-168) and returned in the exact layout
+ * rimdp_model_desc takes (colptr widened to int64).  Entry/column-sum checks
+ * (interval.hpp:132-179) happen at upload.  Failures are RIMDP_ERR_MISSING_FILE
+ * or RIMDP_ERR_SCHEMA with the reference's "<path>: <reason>" message.
+ * Two-phase: read returns sizes and an opaque host handle, take copies the
+ * arrays into caller buffers (any may be NULL), free releases the handle. */
+typedef struct rimdp_native_sizes {
+    int32_t num_states;
+    int32_t num_cols;
+    int64_t nnz;            /* after alignment and [0,0] removal */
+    int32_t imdp;           /* 1: model = imdp, 0: imc (one action "0" per state) */
+    int64_t label_bytes;    /* action labels, each NUL-terminated, concatenated */
+} rimdp_native_sizes;
+
+int rimdp_native_read(const char* path, int32_t dtype, rimdp_native_sizes* sizes, void** handle);
+int rimdp_native_take(void* handle, int32_t* stateptr, int64_t* colptr, int32_t* rowval, void* lower, void* upper,
+                      char* labels);
+void rimdp_native_free(void* handle);
 
 /* ---- value iteration ---------------------------------------------------
  * One POD plan per solve, the marshalled form of detail::IterationPlan

@@ -962,6 +962,9 @@ int rimdp_last_error_info(rimdp_error_info* out) {
 
 int rimdp_abi_version(void) { return RIMDP_B200_ABI_VERSION; }
 
+/* Error hook for the host-only translation units (native_io.cpp). */
+int rimdp_internal_fail(int status, const char* msg) { return fail(status, "%s", msg); }
+
 int rimdp_device_count(int* count) {
     if (!count) return fail(RIMDP_ERR_INVALID_ARGUMENT, "count is null");
     int c = 0;
