@@ -175,6 +175,33 @@ class Model:
             raise OracleError(st, err)
         return cls("ref", h, dtype)
 
+    @classmethod
+    def read_native(cls, path, dtype=np.float64):
+        """io::read_native_model (io/native.hpp:457-561) of the reference; ref only."""
+        L = _lib("ref")
+        h = C.c_void_p()
+        err = Err()
+        st = L.fn("read_native", dtype)(os.fsencode(path), C.byref(h), C.byref(err))
+        if st:
+            raise OracleError(st, err)
+        return cls("ref", h, dtype)
+
+    def write_native(self, path, json_debug=False):
+        """io::write_native_model (io/native.hpp:424-455); ref models only."""
+        err = Err()
+        st = self.L.fn("write_native", self.dtype)(self.h, os.fsencode(path), int(json_debug), C.byref(err))
+        if st:
+            raise OracleError(st, err)
+
+    def labels(self):
+        """The model's action labels (IntervalMDP::actions, imdp.hpp:108); ref models only."""
+        f = self.L.fn("model_labels", self.dtype)
+        f.restype = C.c_longlong
+        nb = f(self.h, None)
+        buf = C.create_string_buffer(max(int(nb), 1))
+        f(self.h, buf)
+        return [x.decode() for x in buf.raw[:nb].split(b"\0")[:-1]]
+
     def sizes(self):
         n, nc, nnz = C.c_int(), C.c_int(), C.c_longlong()
         self.L.fn("model_sizes", self.dtype)(self.h, C.byref(n), C.byref(nc), C.byref(nnz))

@@ -16,7 +16,9 @@
 //   omaximize_sequential                 omax.hpp:98-112
 //   oracle::robust_expectation (LP)      tests/oracle.hpp:28-80
 //   oracle::random_feasible_column       tests/oracle.hpp:193-217
+//   io::write_native_model / read_native_model  io/native.hpp:424-561
 
+#include "rimdp/io/native.hpp"
 #include "rimdp/random_model.hpp"
 #include "rimdp/solver.hpp"
 #include "oracle.hpp" // proj/tests/oracle.hpp
@@ -213,6 +215,41 @@ void model_export(void* h, int* stateptr, int* colptr, int* rowval, V* lower, V*
 }
 
 template <class V>
+int write_native(void* h, const char* path, int json_debug, ref_err* err) {
+    ErrOut e{err ? err->msg : nullptr, err ? 512 : 0, nullptr, nullptr, nullptr, nullptr};
+    return guarded(e, [&] {
+        rimdp::io::write_native_model(path, static_cast<Model<V>*>(static_cast<ModelBase*>(h))->mdp, json_debug != 0);
+    });
+}
+
+template <class V>
+int read_native(const char* path, void** out, ref_err* err) {
+    ErrOut e{err ? err->msg : nullptr, err ? 512 : 0, nullptr, nullptr, nullptr, nullptr};
+    return guarded(e, [&] {
+        auto m = new Model<V>;
+        try {
+            m->mdp = rimdp::io::read_native_model<V>(path);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = static_cast<ModelBase*>(m);
+    });
+}
+
+// action labels, each NUL-terminated, concatenated; returns the byte count
+template <class V>
+long long model_labels(void* h, char* out) {
+    const auto& mdp = static_cast<Model<V>*>(static_cast<ModelBase*>(h))->mdp;
+    long long n = 0;
+    for (const auto& a : mdp.actions()) {
+        if (out) std::memcpy(out + n, a.c_str(), a.size() + 1);
+        n += static_cast<long long>(a.size()) + 1;
+    }
+    return n;
+}
+
+template <class V>
 int solve(void* h, const ref_spec* sp, int synthesize, V* values, V* residual,
           long long* iterations, int* policy_cols, V* trace, long long trace_cap, ref_err* err) {
     ErrOut e{err ? err->msg : nullptr, err ? 512 : 0, err ? reinterpret_cast<std::int64_t*>(&err->iterations) : nullptr,
@@ -373,6 +410,13 @@ void ref_model_export_f64(void* h, int* sp, int* cp, int* rv, double* lo, double
 void ref_model_export_f32(void* h, int* sp, int* cp, int* rv, float* lo, float* up) {
     model_export<float>(h, sp, cp, rv, lo, up);
 }
+
+int ref_write_native_f64(void* h, const char* path, int json, ref_err* err) { return write_native<double>(h, path, json, err); }
+int ref_write_native_f32(void* h, const char* path, int json, ref_err* err) { return write_native<float>(h, path, json, err); }
+int ref_read_native_f64(const char* path, void** out, ref_err* err) { return read_native<double>(path, out, err); }
+int ref_read_native_f32(const char* path, void** out, ref_err* err) { return read_native<float>(path, out, err); }
+long long ref_model_labels_f64(void* h, char* out) { return model_labels<double>(h, out); }
+long long ref_model_labels_f32(void* h, char* out) { return model_labels<float>(h, out); }
 
 int ref_solve_f64(void* h, const ref_spec* sp, int synth, double* v, double* res, long long* it,
                   int* pol, double* trace, long long cap, ref_err* err) {

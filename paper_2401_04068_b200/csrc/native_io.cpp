@@ -19,12 +19,15 @@
 //     IntervalProbabilities::align (interval.hpp:218-252) and the removal of
 //     [0, 0] entries (interval.hpp:261-279);
 //   * IntervalMDP::validate's structure checks (imdp.hpp:129-168).
-// Entry and column-sum checks (interval.hpp:132-179) run on the device at
-// upload (rimdp_model_validate).  Every failure is a SchemaViolation whose
-// message is "<path>: <reason>" as in the reference.
+//   * the entry and column-sum checks of IntervalProbabilities::validate
+//     (interval.hpp:132-179) on the aligned pattern, before [0,0] removal.
+// Every failure is a SchemaViolation whose message is "schema violation:
+// <path>: <reason>" as in the reference (errors.hpp:92-95).  The JSON debug
+// variant of the container is not read here (text parsing is out of scope).
 #include "rimdp_b200.h"
 
 #include <charconv>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -74,14 +77,14 @@ public:
     }
     void bytes(void* p, size_t n) {
         in_.read(static_cast<char*>(p), static_cast<std::streamsize>(n));
-        if (static_cast<size_t>(in_.gcount()) != n) fail("truncated file");
+        if (static_cast<size_t>(in_.gcount()) != n) fail("unexpected end of file");
     }
     uint8_t u8() { uint8_t v; bytes(&v, 1); return v; }
     uint32_t u32() { uint32_t v; bytes(&v, 4); return v; }
     uint64_t u64() { uint64_t v; bytes(&v, 8); return v; }
     std::string str() {
         const uint32_t n = u32();
-        if (n > (1u << 30)) fail("string length implausibly large");
+        if (n > (1u << 28)) fail("string length implausibly large");
         std::string s(n, '\0');
         if (n) bytes(s.data(), n);
         return s;
@@ -91,6 +94,14 @@ private:
     std::string path_;
     std::ifstream in_;
 };
+
+// NumericTraits<V>::to_string (numeric.hpp:31-35): shortest round-trip form
+template <class V>
+std::string num(V v) {
+    char buf[64];
+    auto r = std::to_chars(buf, buf + sizeof buf, v);
+    return std::string(buf, r.ptr);
+}
 
 template <class V>
 struct Model {
@@ -229,7 +240,11 @@ std::unique_ptr<Model<V>> read_model(const std::string& path) {
     };
     structural(lcp, lrv, lnz.size());
     structural(ucp, urv, unz.size());
-    // align (interval.hpp:218-252), then drop [0, 0] entries (:261-279)
+    // align (interval.hpp:218-252), check every entry and column sum of the
+    // aligned pattern (IntervalProbabilities::validate, interval.hpp:132-179,
+    // first violation wins as in check_or_throw :255-258), then drop [0, 0]
+    // entries (:261-279).  Done column by column: the report is column-major.
+    const V tol = sizeof(V) == 8 ? V(1e-9) : V(1e-5f); // NumericTraits feasibility_tolerance (numeric.hpp:53-81)
     m->colptr.reserve(ncols + 1);
     m->colptr.push_back(0);
     m->rowval.reserve(urv.size());
@@ -237,6 +252,7 @@ std::unique_ptr<Model<V>> read_model(const std::string& path) {
     m->upper.reserve(urv.size());
     for (int64_t j = 0; j < ncols; ++j) {
         int64_t a = lcp[j], ae = lcp[j + 1], b = ucp[j], be = ucp[j + 1];
+        V lo_sum(0), up_sum(0);
         while (a < ae || b < be) {
             const int32_t ra = a < ae ? lrv[a] : INT32_MAX, rb = b < be ? urv[b] : INT32_MAX;
             int32_t r;
@@ -244,11 +260,22 @@ std::unique_ptr<Model<V>> read_model(const std::string& path) {
             if (ra < rb) { r = ra; lo = lnz[a++]; up = V(0); }
             else if (rb < ra) { r = rb; lo = V(0); up = unz[b++]; }
             else { r = ra; lo = lnz[a++]; up = unz[b++]; }
+            if (!std::isfinite(lo) || lo < V(0) || lo > V(1))
+                in.model_error("EntryOutOfRange", "lower bound " + num(lo) + " outside [0,1]", -1, j, r);
+            if (!std::isfinite(up) || up < V(0) || up > V(1))
+                in.model_error("EntryOutOfRange", "upper bound " + num(up) + " outside [0,1]", -1, j, r);
+            if (lo > up)
+                in.model_error("BoundOrderViolation", "lower bound " + num(lo) + " exceeds upper bound " + num(up),
+                               -1, j, r);
+            lo_sum += lo;
+            up_sum += up;
             if (lo == V(0) && up == V(0)) continue;
             m->rowval.push_back(r);
             m->lower.push_back(lo);
             m->upper.push_back(up);
         }
+        if (lo_sum > V(1) + tol) in.model_error("InfeasibleColumn", "lower bounds sum to " + num(lo_sum) + " > 1", -1, j);
+        if (up_sum < V(1) - tol) in.model_error("InfeasibleColumn", "upper bounds sum to " + num(up_sum) + " < 1", -1, j);
         m->colptr.push_back(static_cast<int64_t>(m->rowval.size()));
     }
     // IntervalMDP structure (imdp.hpp:129-168): the first violation of the report
@@ -265,6 +292,7 @@ std::unique_ptr<Model<V>> read_model(const std::string& path) {
     if (static_cast<int64_t>(m->labels.size()) != ncols) in.model_error(SE, "one action label required per column");
     for (int64_t s = 0; s < nst; ++s) {
         if (sp[s + 1] <= sp[s]) in.model_error("EmptyActionSet", "state has no actions", s);
+        if (sp[s + 1] > static_cast<int64_t>(m->labels.size())) continue;
         std::unordered_set<std::string> seen;
         for (int32_t c = sp[s]; c < sp[s + 1]; ++c)
             if (!seen.insert(m->labels[c]).second)

@@ -16,7 +16,8 @@ import numpy as np
 from . import build as _build
 
 RIMDP_F64, RIMDP_F32 = 0, 1
-OK, ERR_INVALID_ARGUMENT, ERR_INFEASIBLE_COLUMN, ERR_NON_CONVERGENCE, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE, ERR_INTERNAL = range(8)
+(OK, ERR_INVALID_ARGUMENT, ERR_INFEASIBLE_COLUMN, ERR_NON_CONVERGENCE, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE, ERR_INTERNAL,
+ ERR_MISSING_FILE, ERR_SCHEMA) = range(10)
 
 
 class EngineError(RuntimeError):
@@ -104,6 +105,9 @@ _SIGNATURES = {
     "rimdp_bellman_step": ([_VP, _VP, _I32, _I32, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_column_values": ([_VP, _VP, _I32, _VP], C.c_int),
     "rimdp_generate_host": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
+    "rimdp_native_read": ([C.c_char_p, _I32, _VP, _VP], C.c_int),
+    "rimdp_native_take": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
+    "rimdp_native_free": ([_VP], None),
     "rimdp_random_imdp": ([_I32, _I32, _D, _D, C.c_uint64, _I32, _I32, _VP, _VP], C.c_int),
     "rimdp_random_imdp_take": ([_VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
 }
@@ -210,6 +214,35 @@ def generate_host(cfg: GenConfig):
     return sp, cp, rv, lo, up
 
 
+class NativeSizes(C.Structure):
+    _fields_ = [("num_states", C.c_int32), ("num_cols", C.c_int32), ("nnz", C.c_int64), ("imdp", C.c_int32),
+                ("label_bytes", C.c_int64)]
+
+
+def read_native_model(path, dtype=np.float64):
+    """An IMDPCSC1 model container as the engine's CSC arrays (rimdp_native_read;
+    the reference's io::read_native_model, io/native.hpp:457-561):
+    (stateptr int32, colptr int64, rowval int32, lower, upper, labels list[str]).
+    Raises EngineError with status ERR_MISSING_FILE / ERR_SCHEMA and the
+    reference's message on a bad container."""
+    lib = load()
+    sz = NativeSizes()
+    h = C.c_void_p()
+    _check(lib.rimdp_native_read(os.fsencode(path), _dt(dtype), C.byref(sz), C.byref(h)))
+    try:
+        sp = np.empty(sz.num_states + 1, np.int32)
+        cp = np.empty(sz.num_cols + 1, np.int64)
+        rv = np.empty(sz.nnz, np.int32)
+        lo = np.empty(sz.nnz, dtype)
+        up = np.empty(sz.nnz, dtype)
+        lab = C.create_string_buffer(max(int(sz.label_bytes), 1))
+        _check(lib.rimdp_native_take(h, _p(sp), _p(cp), _p(rv), _p(lo), _p(up), lab))
+    finally:
+        lib.rimdp_native_free(h)
+    labels = [x.decode() for x in lab.raw[:sz.label_bytes].split(b"\0")[:-1]]
+    return sp, cp, rv, lo, up, labels
+
+
 def _dt(dtype) -> int:
     return RIMDP_F64 if np.dtype(dtype) == np.float64 else RIMDP_F32
 
@@ -263,6 +296,12 @@ class DeviceModel:
         h = C.c_void_p()
         _check(load().rimdp_model_create_shard(C.byref(d), int(state_begin), int(num_global_states), C.byref(h)))
         return cls(h, dtype)
+
+    @classmethod
+    def from_native(cls, path, dtype=np.float64, device: int = 0) -> "DeviceModel":
+        """Upload an IMDPCSC1 container's CSC arrays directly."""
+        sp, cp, rv, lo, up, _ = read_native_model(path, dtype)
+        return cls.from_csc(sp, cp, rv, lo, up, device=device)
 
     @classmethod
     def generate(cls, cfg: GenConfig) -> "DeviceModel":
