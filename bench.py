@@ -358,7 +358,7 @@ def engine_arm(args, w):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     d2h = values.nbytes + residual.nbytes
-    ref_iters = bit_exact = None
+    ref_iters = bit_exact = sample_diff = None
     gj = os.path.join(ROOT, "tests", "golden", f"{args.config}.json")
     if os.path.exists(gj) and args.dtype == "f64" and w["states"] == WORKLOADS[args.config]["states"]:
         import hashlib
@@ -368,6 +368,8 @@ def engine_arm(args, w):
             ref_iters = run["iterations"]
             bit_exact = (hashlib.sha256(values.tobytes()).hexdigest() == run["values_sha256"] and
                          hashlib.sha256(residual.tobytes()).hexdigest() == run["residual_sha256"])
+            idx = np.array(run["sample_idx"])
+            sample_diff = float(np.abs(values[idx] - np.array([float.fromhex(h) for h in run["sample_hex"]])).max())
     m.close()
     clk.__exit__()
     cpu = None
@@ -408,6 +410,7 @@ def engine_arm(args, w):
                 "h2d_bytes_per_step": h2d / max(e2e_iters, 1), "d2h_bytes_per_step": d2h / max(e2e_iters, 1),
                 "seconds_to_convergence": e2e_s, "iterations": e2e_iters,
                 "reference_iterations": ref_iters, "values_bit_exact_vs_reference": bit_exact,
+                "max_abs_diff_vs_reference_samples": sample_diff,
                 "call": ("DeviceModel.from_csc + problems.value_iteration (C ABI)" if world == 1 else
                          "DeviceModel.from_csc_shard + sharded.ShardedSolver.solve (C ABI + NCCL)")},
         "time_to_convergence_s": e2e_s,

@@ -126,6 +126,8 @@ struct SolveState {
 
 } // namespace
 
+constexpr int kMaxSideStreams = 8;
+
 struct rimdp_model {
     rimdp_dtype dtype = RIMDP_F64;
     int device = 0;
@@ -148,8 +150,14 @@ struct rimdp_model {
     int sm_count = 148;
     int short_blocks_per_sm = 4;
     bool bitonic = false;                     // many-pick long columns: bitonic sort instead of selection
+    bool long_exact = false;                  // few-pick long columns: row-order omax_long (RIMDP_LONG=exact)
     bool bucket = true;                       // columns > 256 entries: value buckets first (RIMDP_BUCKET=0: off)
-    DevBuf fallback;                          // [count, columns...] for omax_bucket -> omax_select
+    DevBuf fallback[kSortedClasses];          // per size class: [count, columns...] for omax_bucket -> omax_select
+    int medium_blocks_per_sm = 3;             // omax_medium occupancy variant (RIMDP_MEDIUM_BLOCKS=4: <= 64 registers)
+    int nstreams = 1;                         // column classes fanned out over this many streams (RIMDP_STREAMS)
+    cudaStream_t side[kMaxSideStreams] = {};  // fork/join streams for concurrent column classes
+    cudaEvent_t fork_ev = nullptr, join_ev[kMaxSideStreams] = {};
+    cudaStream_t ls = nullptr;                // stream the next class launch goes to
     size_t l2_persist = 0;                    // bytes of L2 set aside for the value vector (0: none)
     SolveState s;
 };
@@ -279,6 +287,7 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     }
     const int mode = long_mode();
     m->bitonic = mode == 2;
+    m->long_exact = mode == 1;
     {
         // RIMDP_LONG=select (tests) keeps every many-pick column on the selection kernels
         const char* eb = getenv("RIMDP_BUCKET");
@@ -392,6 +401,13 @@ void init_common(rimdp_model* m, int device) {
     CK(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
     if (const char* e = getenv("RIMDP_SHORT_BLOCKS")) m->short_blocks_per_sm = atoi(e) == 5 ? 5 : 4;
+    if (const char* e = getenv("RIMDP_MEDIUM_BLOCKS")) m->medium_blocks_per_sm = atoi(e) == 4 ? 4 : 3;
+    if (const char* e = getenv("RIMDP_STREAMS")) m->nstreams = std::min(std::max(atoi(e), 1), kMaxSideStreams);
+    if (m->nstreams > 1) {
+        for (int i = 0; i < m->nstreams; ++i) CK(cudaStreamCreateWithFlags(&m->side[i], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&m->fork_ev, cudaEventDisableTiming));
+        for (int i = 0; i < m->nstreams; ++i) CK(cudaEventCreateWithFlags(&m->join_ev[i], cudaEventDisableTiming));
+    }
 }
 
 // L2 residency of the gathered value vector: when
@@ -508,7 +524,7 @@ void launch_sorted_class(rimdp_model* m, int count, const DevBuf& list, const T*
         configured[dev] = true;
     }
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
-    k<<<blocks, Sh::threads, smem, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    k<<<blocks, Sh::threads, smem, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                                 m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
 }
 
@@ -528,7 +544,7 @@ void launch_select_class(rimdp_model* m, int count, const int* list, const T* V,
         configured[dev] = true;
     }
     const int blocks = grid_for(count, Sh::Groups, m->sm_count, per_sm[dev]);
-    k<<<blocks, Sh::Block, smem, m->stream>>>(count, list, m->colptr.as<long long>(), m->rows.as<int>(),
+    k<<<blocks, Sh::Block, smem, m->ls>>>(count, list, m->colptr.as<long long>(), m->rows.as<int>(),
                                               m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl,
                                               count_dev);
 }
@@ -549,12 +565,13 @@ void launch_bucket_class(rimdp_model* m, int count, const DevBuf& list, const T*
         per_sm[dev] = std::max(per_sm[dev], 1);
         configured[dev] = true;
     }
-    m->fallback.ensure(sizeof(int) * (size_t)(std::max(count, 1) + 1));
-    int* nfb = m->fallback.as<int>();
+    DevBuf& fbuf = m->fallback[LG - kSortedMinLog];
+    fbuf.ensure(sizeof(int) * (size_t)(std::max(count, 1) + 1));
+    int* nfb = fbuf.as<int>();
     int* fb = nfb + 1;
-    CK(cudaMemsetAsync(nfb, 0, sizeof(int), m->stream));
+    CK(cudaMemsetAsync(nfb, 0, sizeof(int), m->ls));
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
-    k<<<blocks, Sh::NT, smem, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    k<<<blocks, Sh::NT, smem, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                            m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V,
                                            q, ctl, fb, nfb);
     launch_select_class<T, P, LG>(m, count, fb, V, q, ctl, nfb);
@@ -582,15 +599,17 @@ template <class T, int E>
 void launch_medium(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl, bool pess,
                    unsigned* work) {
     using Sh = MediumShape<E>;
-    auto k = pess ? omax_medium<T, true, E> : omax_medium<T, false, E>;
-    static int per_sm[64] = {};
+    const bool four = m->medium_blocks_per_sm == 4;
+    auto k = four ? (pess ? omax_medium<T, true, E, 4> : omax_medium<T, false, E, 4>)
+                  : (pess ? omax_medium<T, true, E> : omax_medium<T, false, E>);
+    static int per_sm[2][64] = {};
     const int dev = m->device & 63;
-    if (!per_sm[dev]) {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, Sh::W * 32, 0));
-        per_sm[dev] = std::max(per_sm[dev], 1);
+    if (!per_sm[four][dev]) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[four][dev], k, Sh::W * 32, 0));
+        per_sm[four][dev] = std::max(per_sm[four][dev], 1);
     }
-    const int blocks = grid_for(count, Sh::B * Sh::W, m->sm_count, per_sm[dev]);
-    k<<<blocks, Sh::W * 32, 0, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    const int blocks = grid_for(count, Sh::B * Sh::W, m->sm_count, per_sm[four][dev]);
+    k<<<blocks, Sh::W * 32, 0, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                              m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl, work);
 }
 
@@ -605,7 +624,7 @@ void launch_tiny(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q
     }
     const int steps = (count + 32 / SEG - 1) / (32 / SEG);
     const int blocks = grid_for(steps, 8 * 4, m->sm_count, per_sm[dev]); // >= 4 steps per warp
-    k<<<blocks, 256, 0, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    k<<<blocks, 256, 0, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                       m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
 }
 
@@ -623,17 +642,48 @@ void launch_long_v(rimdp_model* m, int count, const DevBuf& list, const T* V, T*
         configured_smem[dev] = smem;
     }
     const int blocks = grid_for(count, kWarpsPerBlock * kLongGroup, m->sm_count, per_sm[dev]);
-    k<<<blocks, kWarpsPerBlock * 32, smem, m->stream>>>(count, list.as<int>(), m->colptr.as<long long>(),
+    k<<<blocks, kWarpsPerBlock * 32, smem, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(),
                                                           m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
                                                           m->rem.as<T>(), V, m->n_global, q, ctl);
 }
 
-// Exact long columns; the value vector is staged in shared memory when it is
-// small (kLongVsMaxBytes) and the columns are long enough to amortise it.
+template <class T, bool P, bool VS>
+void launch_long_tree_v(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
+    auto k = omax_long_tree<T, P, VS>;
+    const size_t smem = VS ? sizeof(T) * (size_t)m->n_global : 0;
+    static int per_sm[64] = {};
+    static size_t configured_smem[64] = {};
+    const int dev = m->device & 63;
+    if (!per_sm[dev] || configured_smem[dev] != smem) {
+        if (VS) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, kWarpsPerBlock * 32, smem));
+        per_sm[dev] = std::max(per_sm[dev], 1);
+        configured_smem[dev] = smem;
+    }
+    const int blocks = grid_for(count, kWarpsPerBlock, m->sm_count, per_sm[dev]);
+    k<<<blocks, kWarpsPerBlock * 32, smem, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(),
+                                                     m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
+                                                     m->rem.as<T>(), V, m->n_global, q, ctl);
+}
+
+// Few-pick long columns: the single-pass tree-order kernel by default, the
+// row-order (bit-exact) omax_long with RIMDP_LONG=exact.  The value vector
+// is staged in shared memory when it is small (kLongVsMaxBytes) and the
+// columns are long enough to amortise it.
 template <class T>
 void launch_long(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl, bool pess) {
     const bool vs = sizeof(T) * (size_t)m->n_global <= (size_t)kLongVsMaxBytes &&
                     (long long)count * 64 >= (long long)m->n_global;
+    if (!m->long_exact) {
+        if (pess) {
+            if (vs) launch_long_tree_v<T, true, true>(m, count, list, V, q, ctl);
+            else launch_long_tree_v<T, true, false>(m, count, list, V, q, ctl);
+        } else {
+            if (vs) launch_long_tree_v<T, false, true>(m, count, list, V, q, ctl);
+            else launch_long_tree_v<T, false, false>(m, count, list, V, q, ctl);
+        }
+        return;
+    }
     if (pess) {
         if (vs) launch_long_v<T, true, true>(m, count, list, V, q, ctl);
         else launch_long_v<T, true, false>(m, count, list, V, q, ctl);
@@ -643,26 +693,91 @@ void launch_long(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q
     }
 }
 
+// Fork/join over the side streams: independent column classes (they write
+// disjoint entries of q) run concurrently, so the latency-bound phases and
+// launch tails of one class overlap the loads of another.
+struct ClassFanout {
+    rimdp_model* m;
+    int used = 0, next = 0;
+    bool on;
+    ClassFanout(rimdp_model* mm, int classes) : m(mm), on(mm->nstreams > 1 && classes > 1) {
+        m->ls = m->stream;
+        if (on) CK(cudaEventRecord(m->fork_ev, m->stream));
+    }
+    void pick() {
+        if (!on) return;
+        const int i = next++ % m->nstreams;
+        if (i >= used) {
+            CK(cudaStreamWaitEvent(m->side[i], m->fork_ev, 0));
+            used = i + 1;
+        }
+        m->ls = m->side[i];
+    }
+    ~ClassFanout() noexcept(false) {
+        if (on)
+            for (int i = 0; i < used; ++i) {
+                CK(cudaEventRecord(m->join_ev[i], m->side[i]));
+                CK(cudaStreamWaitEvent(m->stream, m->join_ev[i], 0));
+            }
+        m->ls = m->stream;
+    }
+};
+
+int column_classes(const ColumnLists& L) {
+    int k = (L.n_short > 0) + (L.n_exact > 0) + (L.n_medium[0] > 0) + (L.n_medium[1] > 0);
+    for (int i = 0; i < 3; ++i) k += L.n_tiny[i] > 0;
+    for (int i = 0; i < kSortedClasses; ++i) k += L.n_sorted[i] > 0;
+    return k;
+}
+
+template <class T, bool P, int LG = kSortedMaxLog>
+void launch_sorted_fanout(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl, ClassFanout& f) {
+    // longest classes first: they dominate and should start earliest
+    if constexpr (LG >= kSortedMinLog) {
+        const int i = LG - kSortedMinLog;
+        if (L.n_sorted[i] > 0) {
+            f.pick();
+            if (m->bitonic)
+                launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+            else if (LG >= 9 && m->bucket)
+                launch_bucket_class<T, P, (LG >= 9 ? LG : 9)>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+            else
+                launch_select_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i].as<int>(), V, q, ctl);
+        }
+        launch_sorted_fanout<T, P, LG - 1>(m, L, V, q, ctl, f);
+    }
+}
+
 // Per-column expectations q for the columns of one set of class lists.
 template <class T>
 void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
+    ClassFanout f(m, column_classes(L));
+    if (f.on) {
+        if (pess)
+            launch_sorted_fanout<T, true>(m, L, V, q, ctl, f);
+        else
+            launch_sorted_fanout<T, false>(m, L, V, q, ctl, f);
+    }
     if (L.n_short > 0) {
+        f.pick();
         const int blocks = grid_for(L.n_short, kShortBatch * kWarpsPerBlock, m->sm_count, 5);
         auto k = pess ? omax_short<T, true> : omax_short<T, false>;
-        k<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(L.n_short, L.short_list.as<int>(), m->colptr.as<long long>(),
-                                                          m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
-                                                          m->rem.as<T>(), V, q, ctl, work);
+        k<<<blocks, kWarpsPerBlock * 32, 0, m->ls>>>(L.n_short, L.short_list.as<int>(), m->colptr.as<long long>(),
+                                                      m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
+                                                      m->rem.as<T>(), V, q, ctl, work);
     }
-    if (L.n_tiny[0] > 0) launch_tiny<T, 4>(m, L.n_tiny[0], L.tiny_list[0], V, q, ctl, pess);
-    if (L.n_tiny[1] > 0) launch_tiny<T, 8>(m, L.n_tiny[1], L.tiny_list[1], V, q, ctl, pess);
-    if (L.n_tiny[2] > 0) launch_tiny<T, 16>(m, L.n_tiny[2], L.tiny_list[2], V, q, ctl, pess);
-    if (L.n_medium[0] > 0) launch_medium<T, 2>(m, L.n_medium[0], L.medium_list[0], V, q, ctl, pess, work + 2);
-    if (L.n_medium[1] > 0) launch_medium<T, 4>(m, L.n_medium[1], L.medium_list[1], V, q, ctl, pess, work + 3);
-    if (L.n_exact > 0) launch_long<T>(m, L.n_exact, L.exact_list, V, q, ctl, pess);
-    if (pess)
-        launch_sorted<T, true>(m, L, V, q, ctl);
-    else
-        launch_sorted<T, false>(m, L, V, q, ctl);
+    if (L.n_medium[0] > 0) { f.pick(); launch_medium<T, 2>(m, L.n_medium[0], L.medium_list[0], V, q, ctl, pess, work + 2); }
+    if (L.n_medium[1] > 0) { f.pick(); launch_medium<T, 4>(m, L.n_medium[1], L.medium_list[1], V, q, ctl, pess, work + 3); }
+    if (L.n_exact > 0) { f.pick(); launch_long<T>(m, L.n_exact, L.exact_list, V, q, ctl, pess); }
+    if (L.n_tiny[2] > 0) { f.pick(); launch_tiny<T, 16>(m, L.n_tiny[2], L.tiny_list[2], V, q, ctl, pess); }
+    if (L.n_tiny[1] > 0) { f.pick(); launch_tiny<T, 8>(m, L.n_tiny[1], L.tiny_list[1], V, q, ctl, pess); }
+    if (L.n_tiny[0] > 0) { f.pick(); launch_tiny<T, 4>(m, L.n_tiny[0], L.tiny_list[0], V, q, ctl, pess); }
+    if (!f.on) {
+        if (pess)
+            launch_sorted<T, true>(m, L, V, q, ctl);
+        else
+            launch_sorted<T, false>(m, L, V, q, ctl);
+    }
 }
 
 // One Bellman iteration: [q path for long states: column kernels] ->
@@ -1048,6 +1163,11 @@ int rimdp_model_destroy(rimdp_model* m) {
         if (m->stream) cudaStreamSynchronize(m->stream);
         m->s.~SolveState();
         new (&m->s) SolveState();
+        for (int i = 0; i < kMaxSideStreams; ++i) {
+            if (m->side[i]) cudaStreamDestroy(m->side[i]);
+            if (m->join_ev[i]) cudaEventDestroy(m->join_ev[i]);
+        }
+        if (m->fork_ev) cudaEventDestroy(m->fork_ev);
         if (m->stream) cudaStreamDestroy(m->stream);
         m->stream = nullptr;
     }

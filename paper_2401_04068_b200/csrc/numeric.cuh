@@ -30,6 +30,12 @@ struct Num<double> {
         b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
         return pessimistic ? b : ~b;
     }
+    // Inverse of key (a key of -0.0 gives +0.0).
+    __device__ __forceinline__ static double value(Bits k, bool pessimistic) {
+        if (!pessimistic) k = ~k;
+        k = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+        return __longlong_as_double(static_cast<long long>(k));
+    }
     // Non-negative residuals compare like their bit patterns.
     __device__ __forceinline__ static unsigned long long res_bits(double r) {
         return static_cast<unsigned long long>(__double_as_longlong(r));
@@ -53,6 +59,11 @@ struct Num<float> {
         Bits b = static_cast<Bits>(__float_as_int(v == 0.0f ? 0.0f : v));
         b = (b >> 31) ? ~b : (b | 0x80000000u);
         return pessimistic ? b : ~b;
+    }
+    __device__ __forceinline__ static float value(Bits k, bool pessimistic) {
+        if (!pessimistic) k = ~k;
+        k = (k >> 31) ? (k & 0x7fffffffu) : ~k;
+        return __int_as_float(static_cast<int>(k));
     }
     __device__ __forceinline__ static unsigned long long res_bits(float r) {
         return static_cast<unsigned long long>(static_cast<unsigned>(__float_as_int(r)));

@@ -458,8 +458,8 @@ struct MediumShape {
     static constexpr int Len = 32 * E;
 };
 
-template <class T, bool kPess, int E>
-__global__ void __launch_bounds__(MediumShape<E>::W * 32)
+template <class T, bool kPess, int E, int kMinBlocks = 1>
+__global__ void __launch_bounds__(MediumShape<E>::W * 32, kMinBlocks)
 omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
             const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl,
@@ -911,6 +911,175 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
         }
         if (lane < ng) q[mc] = acc;
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Long columns with few greedy picks, single pass (the default for class-1
+// columns; RIMDP_LONG=exact keeps the bit-exact omax_long above).
+//
+// One warp per column, one coalesced pass over (row, lower, gap) with U
+// chunks of 32 entries in flight per lane.  During the pass every lane keeps
+// its running sum of V[row] * lower (its own positions, in row order) and its
+// kLongTopK smallest (order key, position, gap); the greedy then pops the
+// lanes' list heads with exact warp argmins (omax.hpp:98-112), as omax_long's
+// phase A, and adds V_j * min(g_j, avail) for each pick — V_j is recovered
+// exactly from the order key.  A lane that runs dry while owning unseen
+// positions switches the warp to full rescans (rows and gaps only).
+//   q = sum_lanes(sum V l) + sum_picks V_j min(g_j, avail_j)
+// So the column data crosses HBM exactly once (omax_long reads rows and
+// lower twice to sum the products in row order).  The sum is in lane/tree
+// order instead of the reference's row order: within a few ulps (north_star:
+// 1e-12 per iteration), deterministic.  The picks, hence the cut, are exact.
+template <class T, bool kPess, bool kVs>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+omax_long_tree(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+               const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+               const T* __restrict__ rem, const T* __restrict__ Vg, int nv, T* __restrict__ q,
+               const Ctl* __restrict__ ctl) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    constexpr int K = kLongTopK, U = 4;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    extern __shared__ __align__(16) unsigned char vs_raw[];
+    const T* __restrict__ V = Vg;
+    if constexpr (kVs) {
+        T* vs = reinterpret_cast<T*>(vs_raw);
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) vs[i] = __ldg(Vg + i);
+        __syncthreads();
+        V = vs;
+    }
+    const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
+    for (int item = gw; item < nlist; item += nw) {
+        const int c = __ldg(list + item);
+        const long long b = __ldg(colptr + c);
+        const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
+        const T r = __ldg(rem + c);
+        Bits hk[K];
+        int hp[K];
+        T hg[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+            hk[t] = ~Bits(0);
+            hp[t] = INT_MAX;
+            hg[t] = T(0);
+        }
+        int seen = 0;
+        T acc = T(0);
+        for (int j0 = 0; j0 < L; j0 += 32 * U) {
+            int rw[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u * 32 + lane;
+                rw[u] = j < L ? ld_hint(rows + b + j, pstream) : 0;
+            }
+            T ll[U], gg[U], vv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u * 32 + lane;
+                ll[u] = j < L ? ld_hint(lower + b + j, pstream) : T(0);
+                gg[u] = j < L ? ld_hint(gap + b + j, pstream) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u * 32 + lane;
+                if constexpr (kVs) vv[u] = j < L ? V[rw[u]] : T(0);
+                else vv[u] = j < L ? ld_hint(V + rw[u], pval) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u * 32 + lane;
+                if (j < L) {
+                    ++seen;
+                    acc = N::add(acc, N::mul(vv[u], ll[u]));
+                    const Bits k = N::key(vv[u], kPess);
+                    if (k < hk[K - 1]) {
+                        Bits ck = k;
+                        int cp = j;
+                        T cg = gg[u];
+#pragma unroll
+                        for (int t = 0; t < K; ++t) {
+                            if (ck < hk[t] || (ck == hk[t] && cp < hp[t])) {
+                                const Bits tk = hk[t];
+                                const int tp = hp[t];
+                                const T tg = hg[t];
+                                hk[t] = ck;
+                                hp[t] = cp;
+                                hg[t] = cg;
+                                ck = tk;
+                                cp = tp;
+                                cg = tg;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = N::add(acc, __shfl_xor_sync(kFull, acc, o));
+        // greedy along the adversary ordering (omax.hpp:98-112)
+        T extra = T(0), consumed = T(0);
+        bool any = false;
+        Bits lastk = 0;
+        int lastp = -1, popped = 0;
+        bool dry = false;
+        for (;;) {
+            const T avail = N::sub(r, consumed);
+            if (!(avail > T(0))) break;
+            if (__any_sync(kFull, dry)) break;
+            Bits mk;
+            int mp;
+            if (!warp_argmin_pos(hk[0], hp[0], hp[0] != INT_MAX, mk, mp)) break;
+            const bool mine = hp[0] == mp;
+            const T g = __shfl_sync(kFull, hg[0], __ffs(__ballot_sync(kFull, mine)) - 1);
+            if (mine) {
+#pragma unroll
+                for (int t = 0; t < K - 1; ++t) {
+                    hk[t] = hk[t + 1];
+                    hp[t] = hp[t + 1];
+                    hg[t] = hg[t + 1];
+                }
+                hk[K - 1] = ~Bits(0);
+                hp[K - 1] = INT_MAX;
+                ++popped;
+                dry = hp[0] == INT_MAX && seen > popped;
+            }
+            extra = N::add(extra, N::mul(N::value(mk, kPess), g < avail ? g : avail));
+            consumed = N::add(consumed, g);
+            any = true;
+            lastk = mk;
+            lastp = mp;
+        }
+        if (__any_sync(kFull, dry)) {
+            for (;;) {
+                const T avail = N::sub(r, consumed);
+                if (!(avail > T(0))) break;
+                Bits bk = ~Bits(0);
+                int bp = INT_MAX;
+                bool have = false;
+                for (int j = lane; j < L; j += 32) {
+                    const Bits k = N::key(V[__ldg(rows + b + j)], kPess);
+                    const bool after = !any || k > lastk || (k == lastk && j > lastp);
+                    if (after && (!have || k < bk || (k == bk && j < bp))) {
+                        bk = k;
+                        bp = j;
+                        have = true;
+                    }
+                }
+                Bits mk;
+                int mp;
+                if (!warp_argmin_pos(bk, bp, have, mk, mp)) break;
+                const T g = __ldg(gap + b + mp);
+                extra = N::add(extra, N::mul(N::value(mk, kPess), g < avail ? g : avail));
+                consumed = N::add(consumed, g);
+                any = true;
+                lastk = mk;
+                lastp = mp;
+            }
+        }
+        if (lane == 0) q[c] = N::add(acc, extra);
     }
 }
 

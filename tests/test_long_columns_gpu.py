@@ -188,3 +188,26 @@ def test_generated_shard_steps_match_whole_model():
         pv, pc = part.bellman_step(v, True, True)
         assert np.array_equal(bits(pv[sb:se]), bits(wv[sb:se]))
         assert np.array_equal(pc + sb * 4, wc[sb:se])
+
+
+@pytest.fixture(scope="module")
+def fewpick():
+    # C3's law at a smaller size: every column has all 400 states as support, few greedy picks
+    return engine.random_imdp(400, 3, 1.0, 1.0 / 400, seed=5)
+
+
+@pytest.mark.parametrize("pess", [True, False])
+@pytest.mark.parametrize("values", ["tricky", "random"])
+def test_single_pass_long_kernel_within_tolerance(fewpick, pess, values):
+    """omax_long_tree (default for few-pick long columns): exact picks, tree-order
+    sums within 1e-13 of the reference; deterministic; RIMDP_LONG=exact stays
+    bit-exact on the same columns."""
+    v = tricky_values(400, 6) if values == "tricky" else np.random.default_rng(9).random(400)
+    ref = ref_columns(fewpick, v, pess)
+    m = engine.DeviceModel.from_csc(*fewpick)
+    assert m.info().mid_columns == m.num_cols  # every column on the few-pick long path
+    q = m.column_values(v, pess)
+    assert np.abs(q - ref).max() <= COL_TOL
+    assert np.array_equal(bits(q), bits(engine.DeviceModel.from_csc(*fewpick).column_values(v, pess)))
+    ex = with_long_mode("exact", lambda: engine.DeviceModel.from_csc(*fewpick))
+    assert np.array_equal(bits(ex.column_values(v, pess)), bits(ref))

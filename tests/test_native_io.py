@@ -246,12 +246,13 @@ def test_native_container_uploads_and_solves_like_the_golden_arrays(tmp_path, go
         n = len(sp) - 1
         cp32 = [int(x) for x in cp]
         attrs = {"model": "imdp", "format": "sparse_csc", "rows": "to", "cols": "from/action", "num_states": str(n)}
-        var = {"lower_colptr": (1, cp32), "lower_rowval": (1, rv), "lower_nzval": (2, lo),
-               "upper_colptr": (1, cp32), "upper_rowval": (1, rv), "upper_nzval": (2, up),
+        code = 2 if lo.dtype == np.float64 else 3
+        var = {"lower_colptr": (1, cp32), "lower_rowval": (1, rv), "lower_nzval": (code, lo),
+               "upper_colptr": (1, cp32), "upper_rowval": (1, rv), "upper_nzval": (code, up),
                "stateptr": (1, sp), "action_vals": (4, [str(i) for i in range(len(cp) - 1)])}
         path = str(tmp_path / f"{name}.imdpcsc")
         write_container(path, attrs, var)
-        m = engine.DeviceModel.from_native(path)
+        m = engine.DeviceModel.from_native(path, dtype=lo.dtype)
         assert (m.num_states, m.num_cols, m.nnz) == (n, len(cp) - 1, int(cp[-1]))
         for key in golden.solves(name):
             meta = golden.meta[key]
