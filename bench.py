@@ -335,7 +335,9 @@ def engine_arm(args, w):
         dist.barrier()
     t = time.perf_counter()
     h2d = sum(np.asarray(v).nbytes for v in kw.values() if isinstance(v, np.ndarray))
-    if world == 1:
+    if args.no_e2e:  # kernel experiments only: no solve to convergence
+        e2e_iters, values, residual = 1, np.zeros(n, dtype), np.zeros(n, dtype)
+    elif world == 1:
         if arrays is not None:
             dm = engine.DeviceModel.from_csc(*arrays, device=local)
             h2d += sum(a.nbytes for a in arrays)
@@ -360,7 +362,7 @@ def engine_arm(args, w):
     d2h = values.nbytes + residual.nbytes
     ref_iters = bit_exact = sample_diff = None
     gj = os.path.join(ROOT, "tests", "golden", f"{args.config}.json")
-    if os.path.exists(gj) and args.dtype == "f64" and w["states"] == WORKLOADS[args.config]["states"]:
+    if os.path.exists(gj) and not args.no_e2e and args.dtype == "f64" and w["states"] == WORKLOADS[args.config]["states"]:
         import hashlib
         with open(gj) as f:
             run = json.load(f)["runs"].get(f"m{int(w['maximize'])}p{int(w['pessimistic'])}")
@@ -514,6 +516,7 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="experiments: skip the end-to-end solve (no e2e number)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak (C2 law, N x the states) or strong (fixed model)")
     args = ap.parse_args()
