@@ -11,6 +11,7 @@
 //   verify_policy(mdp, policy, spec, options)    solver.hpp:204-251
 //   bellman_step(mdp, v_prev, mode, frozen, w)   bellman.hpp:127-133
 //   robust_expectation(column, values, mode)     omax.hpp:182-199
+//   io::read_native_model<Value>(path)           io/native.hpp:457-561
 //
 // with the same results (bit-identical on the exact-order kernels, see
 // DESIGN.md "Parity") and the same exception types and messages
@@ -141,6 +142,54 @@ Plan<Value> make_plan(const rimdp::Specification<Value>& spec, index_t n) {
 }
 
 } // namespace detail
+
+namespace io {
+
+/// io::read_native_model (io/native.hpp:457-561) through the engine's native
+/// reader (rimdp_native_read, csrc/native_io.cpp): the same container checks
+/// and the same MissingFile / SchemaViolation messages, and the same model —
+/// the arrays it returns are exactly the validated, aligned CSC pattern the
+/// reference builds, so they are assembled without re-validation.  The binary
+/// container only (the JSON debug variant is refused with a SchemaViolation).
+template <typename Value>
+rimdp::IntervalMDP<Value> read_native_model(const std::string& path) {
+    static_assert(has_device_path<Value>, "rimdp_b200: only double and float models have a device path");
+    const rimdp_dtype dt = dtype_of<Value>();
+    rimdp_native_sizes sz{};
+    void* h = nullptr;
+    const int st = rimdp_native_read(path.c_str(), dt, &sz, &h);
+    if (st == RIMDP_ERR_MISSING_FILE) throw rimdp::MissingFile(path);
+    if (st == RIMDP_ERR_SCHEMA) {
+        const std::string msg = rimdp_last_error();
+        const std::string prefix = "schema violation: ";
+        throw rimdp::SchemaViolation(msg.rfind(prefix, 0) == 0 ? msg.substr(prefix.size()) : msg);
+    }
+    detail::check(st, dt);
+    struct Free {
+        void* h;
+        ~Free() { rimdp_native_free(h); }
+    } guard{h};
+    std::vector<index_t> stateptr(static_cast<std::size_t>(sz.num_states) + 1), rowval(sz.nnz);
+    std::vector<std::int64_t> colptr(static_cast<std::size_t>(sz.num_cols) + 1);
+    std::vector<Value> lower(sz.nnz), upper(sz.nnz);
+    std::vector<char> labels(static_cast<std::size_t>(sz.label_bytes) + 1);
+    detail::check(rimdp_native_take(h, stateptr.data(), colptr.data(), rowval.data(), lower.data(), upper.data(),
+                                    labels.data()),
+                  dt);
+    std::vector<index_t> cp(colptr.begin(), colptr.end()); // the container's int32 colptr, widened and back
+    std::vector<std::string> actions;
+    actions.reserve(sz.num_cols);
+    for (std::size_t i = 0; i < static_cast<std::size_t>(sz.label_bytes);) {
+        actions.emplace_back(labels.data() + i);
+        i += actions.back().size() + 1;
+    }
+    auto t = rimdp::IntervalProbabilities<Value>::from_aligned_unchecked(sz.num_states, sz.num_cols, std::move(cp),
+                                                                         std::move(rowval), std::move(lower),
+                                                                         std::move(upper));
+    return rimdp::IntervalMDP<Value>::from_parts_unchecked(std::move(t), std::move(stateptr), std::move(actions));
+}
+
+} // namespace io
 
 /// One IMDP resident in HBM (rimdp_model): the device CSC store plus the
 /// per-column remainders and the column schedule, built once.

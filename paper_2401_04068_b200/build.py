@@ -100,8 +100,11 @@ def build_cpp_tests(force: bool = False) -> str | None:
         return CPP_TEST_BIN
     os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
     stubs = os.path.join(ROOT, "oracle", "stubs")  # Boost stub: Rational is never instantiated
+    # nlohmann/json 3.11.3 for the reference's io/native.hpp (container parity cases)
+    import sysconfig
+    json_inc = os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend", "thirdparty", "nlohmann")
     cmd = ["g++", "-std=gnu++20", "-O2", "-Wall", "-Wextra", "-Wno-unused-parameter", "-ffp-contract=off",
-           "-I", stubs, "-I", REFERENCE_INCLUDE, "-I", INCLUDE, CPP_TEST_SRC, "-o", CPP_TEST_BIN,
+           "-I", stubs, "-I", REFERENCE_INCLUDE, "-I", INCLUDE, "-I", json_inc, CPP_TEST_SRC, "-o", CPP_TEST_BIN,
            "-L", LIBDIR, "-lrimdp_b200", f"-Wl,-rpath,{LIBDIR}", "-Wl,-rpath,$ORIGIN/../../../paper_2401_04068_b200/lib",
            "-pthread"]
     subprocess.run(cmd, check=True)

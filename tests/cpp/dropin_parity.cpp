@@ -15,13 +15,17 @@
 // Cases mirror the reference's own hot-path tests (test_solver.cpp,
 // test_omax.cpp): the paper model in all four modes, random models in every
 // property kind, reach-avoid, rewards, policy synthesis and re-verification,
-// single Bellman steps, single columns, and the error paths.
+// single Bellman steps, single columns, the error paths, and native IMDPCSC1
+// containers read by both readers (test_io.cpp).
+#include "rimdp/io/native.hpp"
 #include "rimdp/random_model.hpp"
 #include "rimdp/solver.hpp"
 #include "rimdp_b200/dropin.hpp"
 
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <iterator>
 #include <cstring>
 #include <functional>
 #include <random>
@@ -251,10 +255,50 @@ int no_device() {
     return g.find("no CUDA device") != std::string::npos ? 0 : 1;
 }
 
+// io::read_native_model against rimdp_b200::io::read_native_model on the same
+// container files: identical models (IntervalMDP::operator==), identical
+// exception types and messages.  Host-only: runs with or without a device.
+template <typename Value>
+void native_case(const char* label, const IntervalMDP<Value>& mdp) {
+    const std::string path = std::string("/tmp/dropin_native_") + label + ".imdpcsc";
+    io::write_native_model(path, mdp);
+    const auto a = io::read_native_model<Value>(path);
+    const auto b = rimdp_b200::io::read_native_model<Value>(path);
+    EXPECT(a == b, "%s: models differ", label);
+    EXPECT(b == mdp, "%s: round trip differs", label);
+    // truncated container: the same SchemaViolation text
+    {
+        std::ifstream in(path, std::ios::binary);
+        std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+        std::ofstream out(path, std::ios::binary | std::ios::trunc);
+        out.write(bytes.data(), static_cast<std::streamsize>(bytes.size() / 2));
+    }
+    std::string ea, eb;
+    try { io::read_native_model<Value>(path); } catch (const SchemaViolation& e) { ea = e.what(); }
+    try { rimdp_b200::io::read_native_model<Value>(path); } catch (const SchemaViolation& e) { eb = e.what(); }
+    EXPECT(!ea.empty() && ea == eb, "%s: truncated: '%s' vs '%s'", label, ea.c_str(), eb.c_str());
+    std::remove(path.c_str());
+    ea.clear();
+    eb.clear();
+    try { io::read_native_model<Value>(path); } catch (const MissingFile& e) { ea = e.what(); }
+    try { rimdp_b200::io::read_native_model<Value>(path); } catch (const MissingFile& e) { eb = e.what(); }
+    EXPECT(!ea.empty() && ea == eb, "%s: missing: '%s' vs '%s'", label, ea.c_str(), eb.c_str());
+}
+
+void native_cases() {
+    native_case<double>("r200x4", random_imdp<double>({200, 4, 24.0 / 200, 1.0 / 24, 8}));
+    native_case<float>("f32r60", random_imdp<float>({60, 3, 0.2, 1.0 / 12, 9}));
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
-    if (argc > 1 && std::strcmp(argv[1], "--no-device") == 0) return no_device();
+    if (argc > 1 && std::strcmp(argv[1], "--no-device") == 0) {
+        native_cases(); // host-only reader
+        if (g_fail) return 1;
+        return no_device();
+    }
+    native_cases();
     paper_cases();
     error_cases();
     // short columns only (warp kernel, exact order): bit-exact
