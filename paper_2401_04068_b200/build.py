@@ -50,15 +50,19 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every .cu under csrc into one shared library for sm_100a."""
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: tuple = ()) -> str:
+    """Compile every .cu under csrc into one shared library for sm_100a
+    (`out` / `defines`: an alternative build for kernel experiments)."""
+    if out is None and not force and up_to_date():
         return LIB
+    lib_path = out or LIB
     os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(lib_path), exist_ok=True)
     objs = []
     for src in sources():
         obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC, "-c", src,
+               "-o", obj]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
@@ -72,13 +76,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", *objs, "-o", tmp, "-lcudart"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_path)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib_path
 
 
 CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "dropin_parity.cpp")

@@ -428,7 +428,9 @@ void setup_l2_persistence(rimdp_model* m, size_t value_bytes) {
     if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, m->device) != cudaSuccess ||
         max_persist <= 0)
         return;
-    const size_t want = std::min<size_t>((size_t)max_persist, value_bytes);
+    // RIMDP_L2_PERSIST=1: the whole vector; =P with 2 <= P <= 100: P percent of it
+    const int pct = atoi(e) >= 2 ? std::min(atoi(e), 100) : 100;
+    const size_t want = std::min<size_t>((size_t)max_persist, value_bytes * (size_t)pct / 100);
     if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
         cudaGetLastError();
         return;

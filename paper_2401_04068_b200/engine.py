@@ -130,11 +130,12 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     global _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(_build.LIB):
-                if not build_if_missing:
-                    raise FileNotFoundError(f"engine library not built: {_build.LIB}")
+            path = os.environ.get("RIMDP_B200_LIB", _build.LIB)  # experiments: an alternative in-tree build
+            if not os.path.exists(path):
+                if not build_if_missing or path != _build.LIB:
+                    raise FileNotFoundError(f"engine library not built: {path}")
                 _build.build()
-            lib = C.CDLL(_build.LIB)
+            lib = C.CDLL(path)
             _declare(lib)
             _lib = lib
     return _lib
