@@ -211,3 +211,16 @@ def test_single_pass_long_kernel_within_tolerance(fewpick, pess, values):
     assert np.array_equal(bits(q), bits(engine.DeviceModel.from_csc(*fewpick).column_values(v, pess)))
     ex = with_long_mode("exact", lambda: engine.DeviceModel.from_csc(*fewpick))
     assert np.array_equal(bits(ex.column_values(v, pess)), bits(ref))
+
+
+@pytest.mark.parametrize("pess", [True, False])
+def test_single_pass_long_kernel_f32(fewpick, pess):
+    """The f32 store of the same few-pick columns (NumericTraits<float>, tol 1e-5)."""
+    sp, cp, rv, lo, up = fewpick
+    arr32 = (sp, cp, rv, lo.astype(np.float32), up.astype(np.float32))
+    v32 = np.random.default_rng(10).random(400).astype(np.float32)
+    ref32 = ref_columns(arr32, v32, pess)
+    q32 = engine.DeviceModel.from_csc(*arr32).column_values(v32, pess)
+    assert np.abs(q32.astype(np.float64) - ref32).max() <= 1e-5
+    ex = with_long_mode("exact", lambda: engine.DeviceModel.from_csc(*arr32))
+    assert np.array_equal(bits(ex.column_values(v32, pess)), bits(ref32.astype(np.float32)))
