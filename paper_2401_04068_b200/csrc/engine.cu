@@ -155,13 +155,15 @@ struct rimdp_model {
     bool bitonic = false;                     // many-pick long columns: bitonic sort instead of selection
     bool long_exact = false;                  // few-pick long columns: row-order omax_long (RIMDP_LONG=exact)
     bool bucket = true;                       // columns > 256 entries: value buckets first (RIMDP_BUCKET=0: off)
-    DevBuf fallback[kSortedClasses];          // per size class: [count, columns...] for omax_bucket -> omax_select
+    DevBuf fallback[kSortedClasses];          // per size class: [count A, count B, columns...] omax_bucket -> omax_select
+    int fallback_parity[kSortedClasses] = {}; // which count the next omax_bucket launch of the class uses
     int medium_blocks_per_sm = 3;             // omax_medium occupancy variant (RIMDP_MEDIUM_BLOCKS=4: <= 64 registers)
     int nstreams = 1;                         // column classes fanned out over this many streams (RIMDP_STREAMS)
     cudaStream_t side[kMaxSideStreams] = {};  // fork/join streams for concurrent column classes
     cudaEvent_t fork_ev = nullptr, join_ev[kMaxSideStreams] = {};
     cudaStream_t ls = nullptr;                // stream the next class launch goes to
     size_t l2_persist = 0;                    // bytes of L2 set aside for the value vector (0: none)
+    bool pdl_now = false;                     // launches of the current iteration use PDL (launch_iteration)
     SolveState s;
 };
 
@@ -296,6 +298,38 @@ void upload_many(int device, cudaStream_t stream, const std::vector<UploadJob>& 
         fail(RIMDP_ERR_CUDA, "staged upload failed: %s", cudaGetErrorString(cudaGetLastError()));
         throw Fail{RIMDP_ERR_CUDA};
     }
+}
+
+// Kernels of the iteration loop are launched with programmatic stream
+// serialization (PDL): a kernel's blocks become resident while its
+// predecessor drains and start with griddepcontrol.wait (pdl_enter), so the
+// launch latency between the column kernels and the action kernel is hidden.
+// It is used when an iteration is at most kPdlMaxKernels launches (C2-C4:
+// 2 launches, 3-4% per iteration on C2); with the dozen column classes of a
+// power-law model it measured slower (C5 f64 4.24 vs 3.25 ms per iteration),
+// so those launch plainly.  RIMDP_PDL=0 launches everything plainly.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("RIMDP_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+template <class... KArgs, class... Args>
+void launch_pdl(bool on, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = on && pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
 int grid_for(long long work, int per_block, int sm_count, int blocks_per_sm) {
@@ -636,7 +670,7 @@ void launch_sorted_class(rimdp_model* m, int count, const DevBuf& list, const T*
         configured[dev] = true;
     }
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
-    k<<<blocks, Sh::threads, smem, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    launch_pdl(m->pdl_now, k, blocks, Sh::threads, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                                 m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
 }
 
@@ -656,7 +690,7 @@ void launch_select_class(rimdp_model* m, int count, const int* list, const T* V,
         configured[dev] = true;
     }
     const int blocks = grid_for(count, Sh::Groups, m->sm_count, per_sm[dev]);
-    k<<<blocks, Sh::Block, smem, m->ls>>>(count, list, m->colptr.as<long long>(), m->rows.as<int>(),
+    launch_pdl(m->pdl_now, k, blocks, Sh::Block, smem, m->ls, count, list, m->colptr.as<long long>(), m->rows.as<int>(),
                                               m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl,
                                               count_dev);
 }
@@ -678,14 +712,21 @@ void launch_bucket_class(rimdp_model* m, int count, const DevBuf& list, const T*
         configured[dev] = true;
     }
     DevBuf& fbuf = m->fallback[LG - kSortedMinLog];
-    fbuf.ensure(sizeof(int) * (size_t)(std::max(count, 1) + 1));
-    int* nfb = fbuf.as<int>();
-    int* fb = nfb + 1;
-    CK(cudaMemsetAsync(nfb, 0, sizeof(int), m->ls));
+    const size_t need = sizeof(int) * (size_t)(std::max(count, 1) + 2);
+    if (fbuf.bytes < need) {
+        fbuf.ensure(need);
+        CK(cudaMemsetAsync(fbuf.p, 0, 2 * sizeof(int), m->ls));
+    }
+    // [count A, count B, columns...]: launches alternate between the two counters
+    int& par = m->fallback_parity[LG - kSortedMinLog];
+    int* nfb = fbuf.as<int>() + par;
+    int* other = fbuf.as<int>() + (par ^ 1);
+    par ^= 1;
+    int* fb = fbuf.as<int>() + 2;
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
-    k<<<blocks, Sh::NT, smem, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    launch_pdl(m->pdl_now, k, blocks, Sh::NT, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                            m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V,
-                                           q, ctl, fb, nfb);
+                                           q, ctl, fb, nfb, other);
     launch_select_class<T, P, LG>(m, count, fb, V, q, ctl, nfb);
 }
 
@@ -721,7 +762,7 @@ void launch_medium(rimdp_model* m, int count, const DevBuf& list, const T* V, T*
         per_sm[four][dev] = std::max(per_sm[four][dev], 1);
     }
     const int blocks = grid_for(count, Sh::B * Sh::W, m->sm_count, per_sm[four][dev]);
-    k<<<blocks, Sh::W * 32, 0, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    launch_pdl(m->pdl_now, k, blocks, Sh::W * 32, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                              m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl, work);
 }
 
@@ -736,7 +777,7 @@ void launch_tiny(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q
     }
     const int steps = (count + 32 / SEG - 1) / (32 / SEG);
     const int blocks = grid_for(steps, 8 * 4, m->sm_count, per_sm[dev]); // >= 4 steps per warp
-    k<<<blocks, 256, 0, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    launch_pdl(m->pdl_now, k, blocks, 256, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                       m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
 }
 
@@ -754,7 +795,7 @@ void launch_long_v(rimdp_model* m, int count, const DevBuf& list, const T* V, T*
         configured_smem[dev] = smem;
     }
     const int blocks = grid_for(count, kWarpsPerBlock * kLongGroup, m->sm_count, per_sm[dev]);
-    k<<<blocks, kWarpsPerBlock * 32, smem, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(),
+    launch_pdl(m->pdl_now, k, blocks, kWarpsPerBlock * 32, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
                                                           m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
                                                           m->rem.as<T>(), V, m->n_global, q, ctl);
 }
@@ -773,7 +814,7 @@ void launch_long_tree_v(rimdp_model* m, int count, const DevBuf& list, const T* 
         configured_smem[dev] = smem;
     }
     const int blocks = grid_for(count, kWarpsPerBlock, m->sm_count, per_sm[dev]);
-    k<<<blocks, kWarpsPerBlock * 32, smem, m->ls>>>(count, list.as<int>(), m->colptr.as<long long>(),
+    launch_pdl(m->pdl_now, k, blocks, kWarpsPerBlock * 32, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
                                                      m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
                                                      m->rem.as<T>(), V, m->n_global, q, ctl);
 }
@@ -874,7 +915,7 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
         f.pick();
         const int blocks = grid_for(L.n_short, kShortBatch * kWarpsPerBlock, m->sm_count, 5);
         auto k = pess ? omax_short<T, true> : omax_short<T, false>;
-        k<<<blocks, kWarpsPerBlock * 32, 0, m->ls>>>(L.n_short, L.short_list.as<int>(), m->colptr.as<long long>(),
+        launch_pdl(m->pdl_now, k, blocks, kWarpsPerBlock * 32, 0, m->ls, L.n_short, L.short_list.as<int>(), m->colptr.as<long long>(),
                                                       m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
                                                       m->rem.as<T>(), V, q, ctl, work);
     }
@@ -895,6 +936,9 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
 // One Bellman iteration: [q path for long states: column kernels] ->
 // [fused bellman_short over the short-state batches] -> [action_reduce over
 // the long states].  The last launch of the three runs the stop test.
+int kernels_per_iteration(const rimdp_model* m);
+constexpr int kPdlMaxKernels = 3;
+
 template <class T>
 void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     SolveState& s = m->s;
@@ -930,6 +974,7 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     a.record_only = s.record_only;
     a.work = s.work.as<unsigned>();
     const T* rw = s.has_rewards ? s.rewards.as<T>() : nullptr;
+    m->pdl_now = kernels_per_iteration(m) <= kPdlMaxKernels && !m->l2_persist && m->nstreams == 1;
     if (m->nbatch > 0) {
         a.finalize = m->nlong_states == 0;
         // occupancy variant: 4 resident blocks (64 registers) or 5 (48 registers)
@@ -937,7 +982,7 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
         const int blocks = grid_for((long long)m->nbatch, kWarpsPerBlock, m->sm_count, bps);
         auto kern = bps == 5 ? (s.pess ? bellman_short<T, true, 5> : bellman_short<T, false, 5>)
                              : (s.pess ? bellman_short<T, true, 4> : bellman_short<T, false, 4>);
-        kern<<<blocks, kWarpsPerBlock * 32, 0, m->stream>>>(
+        launch_pdl(m->pdl_now, kern, blocks, kWarpsPerBlock * 32, 0, m->stream,
             m->nbatch, m->batch_slots.as<int>(), m->batch_states.as<int2>(), m->colptr.as<long long>(),
             m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), vin, vout, rw, (T)s.discount,
             (T)s.eps, a, ctl);
@@ -948,10 +993,11 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     if (ev) CK(cudaEventRecord(ev[2], m->stream));
     if (m->nlong_states > 0) {
         a.finalize = 1;
-        action_reduce<T><<<grid_for(m->nlong_states, 256, m->sm_count, 8), 256, 0, m->stream>>>(
+        launch_pdl(m->pdl_now, action_reduce<T>, grid_for(m->nlong_states, 256, m->sm_count, 8), 256, 0, m->stream,
             a, m->nlong_states, m->long_states.as<int>(), s.q.as<T>(), vin, vout, rw, (T)s.discount, (T)s.eps, ctl);
     }
     if (ev) CK(cudaEventRecord(ev[3], m->stream));
+    m->pdl_now = false;
     CK(cudaGetLastError());
 }
 

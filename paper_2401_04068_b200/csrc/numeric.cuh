@@ -108,4 +108,15 @@ __device__ __forceinline__ int ld_hint(const int* a, unsigned long long pol) {
     return v;
 }
 
+// Programmatic dependent launch: the kernels
+// of an iteration are launched with programmatic stream serialization, so a
+// kernel's blocks can become resident while its predecessor drains.  Every
+// such kernel first waits for the predecessor grid to complete (its writes
+// are then visible), then lets its own successor launch.  Without the launch
+// attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 } // namespace rimdp_dev

@@ -216,6 +216,7 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
            unsigned* __restrict__ work) {
     using N = Num<T>;
     using Bits = typename N::Bits;
+    pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     __shared__ T xs[kWarpsPerBlock][kShortBatch][kShortLen + 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -353,6 +354,7 @@ omax_tiny(int nlist, const int* __restrict__ list, const long long* __restrict__
     using N = Num<T>;
     using Bits = typename N::Bits;
     constexpr int CPW = 32 / SEG;
+    pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     const int lane = threadIdx.x & 31, sg = lane / SEG, sl = lane % SEG;
     const unsigned segmask = (SEG == 32 ? kFull : ((1u << SEG) - 1u)) << (sg * SEG);
@@ -468,6 +470,7 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
     using Bits = typename N::Bits;
     using Sh = MediumShape<E>;
     constexpr int B = Sh::B, W = Sh::W, LEN = Sh::Len;
+    pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     __shared__ T xs[W][B][LEN + 1];
     const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
@@ -684,6 +687,7 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
     using N = Num<T>;
     using Bits = typename N::Bits;
     constexpr int K = kLongTopK, U = 4, G = kLongGroup;
+    pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     constexpr int UB = 2; // phase B: chunks per round
     __shared__ T xs[kWarpsPerBlock][G][32 * UB + 1];
@@ -940,6 +944,7 @@ omax_long_tree(int nlist, const int* __restrict__ list, const long long* __restr
     using N = Num<T>;
     using Bits = typename N::Bits;
     constexpr int K = kLongTopK, U = 4;
+    pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     extern __shared__ __align__(16) unsigned char vs_raw[];
     const T* __restrict__ V = Vg;
@@ -1121,6 +1126,7 @@ omax_sorted(int nlist, const int* __restrict__ list, const long long* __restrict
     using Sh = SortedShape<kLogN>;
     constexpr int N = Sh::N, NT = Sh::threads, E = Sh::E;
     constexpr unsigned long long kPosMask = (1ull << kLogN) - 1;
+    pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     // dynamic shared memory (SortedShape::smem bytes): sort keys (later the
     // available mass by position), gaps by position, warp partials, fix flag
@@ -1379,6 +1385,7 @@ omax_select(int nlist, const int* __restrict__ list, const long long* __restrict
     using N = Num<T>;
     using Bits = typename N::Bits;
     using Sh = SelectShape<LG>;
+    pdl_enter();
     if (nlist_dev) nlist = *nlist_dev; // fallback list of omax_bucket
     constexpr int E = Sh::E, NT = Sh::NT, NW = Sh::NW, LOGE = Sh::LogE;
     constexpr int S = NT < 32 ? NT : 32; // lanes of one column inside a warp
@@ -1655,11 +1662,17 @@ __global__ void __launch_bounds__(BucketShape<LG>::NT, BucketShape<LG>::MinBlock
 omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
             const T* __restrict__ rem, const T* __restrict__ maxgap, const T* __restrict__ V, T* __restrict__ q,
-            const Ctl* __restrict__ ctl, int* __restrict__ fallback, int* __restrict__ nfallback) {
+            const Ctl* __restrict__ ctl, int* __restrict__ fallback, int* __restrict__ nfallback,
+            int* __restrict__ other_nfallback) {
     using N = Num<T>;
     using Bits = typename N::Bits;
     using Sh = BucketShape<LG>;
     constexpr int E = Sh::E, NT = Sh::NT, NW = Sh::NW, B = Sh::B, CAP = kBucketCap;
+    pdl_enter();
+    // fallback counters alternate between launches: this launch counts into
+    // nfallback and clears the other one for the next launch (every earlier
+    // launch, and the selection pass that read it, has completed)
+    if (blockIdx.x == 0 && threadIdx.x == 0) *other_nfallback = 0;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* sv = reinterpret_cast<T*>(smem_raw);                // [Len] V by position
@@ -2133,6 +2146,7 @@ action_reduce(ActionArgs a, int nstates, const int* __restrict__ states, const T
               const T* __restrict__ vin, T* __restrict__ vout, const T* __restrict__ rewards, T discount, T eps,
               Ctl* __restrict__ ctl) {
     using N = Num<T>;
+    pdl_enter();
     if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
     const int* forced = forced_row(a);
     int* chosen = chosen_row(a);
@@ -2185,6 +2199,7 @@ bellman_short(int nbatch, const int* __restrict__ slots, const int2* __restrict_
               const T* __restrict__ rewards, T discount, T eps, ActionArgs a, Ctl* __restrict__ ctl) {
     using N = Num<T>;
     using Bits = typename N::Bits;
+    pdl_enter();
     if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
     __shared__ T xs[kWarpsPerBlock][kShortBatch][kShortLen + 1];
     __shared__ unsigned long long s_res;
