@@ -164,6 +164,9 @@ struct rimdp_model {
     cudaStream_t ls = nullptr;                // stream the next class launch goes to
     size_t l2_persist = 0;                    // bytes of L2 set aside for the value vector (0: none)
     bool pdl_now = false;                     // launches of the current iteration use PDL (launch_iteration)
+    DevBuf vrange;                            // value_range slots [2][min, max] (order keys), for omax_bucket
+    int vrange_parity = 0;
+    const unsigned long long* vrange_cur = nullptr; // slot filled for the current launch_columns
     SolveState s;
 };
 
@@ -726,7 +729,7 @@ void launch_bucket_class(rimdp_model* m, int count, const DevBuf& list, const T*
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
     launch_pdl(m->pdl_now, k, blocks, Sh::NT, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                            m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V,
-                                           q, ctl, fb, nfb, other);
+                                           q, ctl, fb, nfb, other, m->vrange_cur);
     launch_select_class<T, P, LG>(m, count, fb, V, q, ctl, nfb);
 }
 
@@ -902,8 +905,31 @@ void launch_sorted_fanout(rimdp_model* m, const ColumnLists& L, const T* V, T* q
 }
 
 // Per-column expectations q for the columns of one set of class lists.
+// Range of V for the value buckets of omax_bucket: one small launch per
+// column pass, only when a bucket class is scheduled.
+template <class T>
+void launch_value_range(rimdp_model* m, const ColumnLists& L, const T* V) {
+    bool need = false;
+    for (int i = 9 - kSortedMinLog; i < kSortedClasses; ++i) need = need || L.n_sorted[i] > 0;
+    m->vrange_cur = nullptr;
+    if (!need || m->bitonic || !m->bucket) return;
+    if (!m->vrange.p) {
+        m->vrange.ensure(4 * sizeof(unsigned long long));
+        const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+        CK(cudaMemcpyAsync(m->vrange.p, init, sizeof init, cudaMemcpyHostToDevice, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+    }
+    unsigned long long* slot = m->vrange.as<unsigned long long>() + 2 * m->vrange_parity;
+    unsigned long long* other = m->vrange.as<unsigned long long>() + 2 * (m->vrange_parity ^ 1);
+    m->vrange_parity ^= 1;
+    const int n = m->n_global;
+    value_range<T><<<grid_for(n, 256 * 8, m->sm_count, 4), 256, 0, m->stream>>>(n, V, slot, other);
+    m->vrange_cur = slot;
+}
+
 template <class T>
 void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
+    launch_value_range<T>(m, L, V);
     ClassFanout f(m, column_classes(L));
     if (f.on) {
         if (pess)

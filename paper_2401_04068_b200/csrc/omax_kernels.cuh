@@ -1650,20 +1650,76 @@ struct BucketShape {
     static constexpr int MinBlocks = NT >= 1024 ? 1 : 1024 / NT;
     template <class T>
     static constexpr size_t smem() {
-        // V and g by position; hist, cnt (u32 x B); candidates (key, pos, g, V) x kBucketCap; partials;
-        // decision words
-        return 2 * sizeof(T) * (size_t)Len + 2 * 4 * B + kBucketCap * (8 + 4 + 2 * sizeof(T)) +
-               NW * (2 * sizeof(T) + 16) + 64;
+        // hist, cnt (u32 x B) x 2 (alternate columns); candidates (key, pos, g, V) x kBucketCap; partials
+        // (sum g below the bracket, sum V l + V g below) x NW; warp scan totals; decision words x 2
+        return 2 * 2 * 4 * B + kBucketCap * (8 + 4 + 2 * sizeof(T)) + NW * (2 * sizeof(T) + 16) + 64;
     }
 };
 
+// Range of the value vector as order keys of the ascending order (slot
+// [0] = min, [1] = max), for omax_bucket's value buckets.  Launches
+// alternate between two slots; each launch resets the other one.
+template <class T>
+__global__ void __launch_bounds__(256)
+value_range(int n, const T* __restrict__ V, unsigned long long* __restrict__ slot,
+            unsigned long long* __restrict__ other) {
+    using Bits = typename Num<T>::Bits;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        other[0] = ~0ull;
+        other[1] = 0ull;
+    }
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned long long k = static_cast<unsigned long long>(static_cast<Bits>(order_key<T>(__ldg(V + i), true)));
+        lo = k < lo ? k : lo;
+        hi = k > hi ? k : hi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(kFull, lo, o), z = __shfl_xor_sync(kFull, hi, o);
+        lo = a < lo ? a : lo;
+        hi = z > hi ? z : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lo != ~0ull) atomicMin(slot, lo);
+        atomicMax(slot + 1, hi);
+    }
+}
+
+// Many-pick columns of 257 .. 8192 entries: one CTA per column, E = 8
+// entries per thread, kept in registers (no shared-memory staging).
+//
+// Equal-width value buckets of w = +-V (along the adversary order) over the
+// range of the whole value vector (value_range, one launch per iteration:
+// no per-column min/max pass) are monotone in the order (omax.hpp:41-58), so
+// buckets are contiguous and ties share a bucket.  Values outside the range
+// cannot occur; the index is clamped anyway.  A fixed-point gap histogram
+// uses u32 shared atomics at a scale chosen per column so it cannot
+// overflow; it is deterministic.  Since truncation loses < 1 unit per entry,
+// the exact mass before bucket b lies in [F_b, F_b + N_b) (fixed mass and
+// count before b), which brackets the bucket of the cut c (the last entry
+// whose prefix gap mass is < rem) in [b_lo, b_hi]:  b_lo = last non-empty
+// bucket with F_b + N_b <= rem * Sc (certainly reached), b_hi = last
+// non-empty bucket with F_b < rem * Sc.  Entries below b_lo are before c:
+// their exact gap sum (double, tree order) is the base, and their V g is
+// added to the expectation.  The <= kBucketCap entries of [b_lo, b_hi] are
+// resolved exactly by warp 0: bitonic sort by (order key, position),
+// exclusive prefix of the gaps from the base, the cut is the last entry
+// whose prefix is < rem.
+//   q = sum V l + sum_{before c} V g + V_c min(g_c, rem - F(c))
+// A column whose bracket holds more than kBucketCap entries (heavy ties,
+// clustered values) is appended to a fallback list for omax_select.  Sums are
+// in tree order: within a few ulps of the reference (1e-12 tests).
+// Four barriers per column (histogram, scan, bracket, partials); the
+// histogram and the decision words alternate between two buffers so the
+// next column needs no trailing barrier.
 template <class T, bool kPess, int LG>
 __global__ void __launch_bounds__(BucketShape<LG>::NT, BucketShape<LG>::MinBlocks)
 omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
             const T* __restrict__ rem, const T* __restrict__ maxgap, const T* __restrict__ V, T* __restrict__ q,
             const Ctl* __restrict__ ctl, int* __restrict__ fallback, int* __restrict__ nfallback,
-            int* __restrict__ other_nfallback) {
+            int* __restrict__ other_nfallback, const unsigned long long* __restrict__ vrange) {
     using N = Num<T>;
     using Bits = typename N::Bits;
     using Sh = BucketShape<LG>;
@@ -1675,112 +1731,93 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
     if (blockIdx.x == 0 && threadIdx.x == 0) *other_nfallback = 0;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* sv = reinterpret_cast<T*>(smem_raw);                // [Len] V by position
-    T* sgp = sv + Sh::Len;                                  // [Len] gap by position
-    unsigned* hist = reinterpret_cast<unsigned*>(sgp + Sh::Len);
-    unsigned* hcnt = hist + B;
-    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hcnt + B);
+    unsigned* hbuf = reinterpret_cast<unsigned*>(smem_raw);           // [2][hist B | cnt B]
+    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hbuf + 4 * B);
     T* cg = reinterpret_cast<T*>(ckey + CAP);
     T* cv = cg + CAP;
     int* cpos = reinterpret_cast<int*>(cv + CAP);
-    T* pa = reinterpret_cast<T*>(cpos + CAP);   // [NW] partial A
-    T* pb = pa + NW;                            // [NW] partial B
+    T* pa = reinterpret_cast<T*>(cpos + CAP);   // [NW] sum g below the bracket
+    T* pb = pa + NW;                            // [NW] sum V l + sum V g below the bracket
     unsigned long long* wtot = reinterpret_cast<unsigned long long*>(pb + NW); // [2][NW] warp scan totals
-    int* dw = reinterpret_cast<int*>(wtot + 2 * NW); // b_lo + 1, b_hi + 1, -, candidate counter
+    int* dwb = reinterpret_cast<int*>(wtot + 2 * NW); // [2][b_lo + 1, b_hi + 1, -, candidate counter]
     const int t = threadIdx.x, lane = t & 31, wig = t >> 5;
     const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
+    // value range: buckets over [wlo, whi] of w = +-V
+    const T vmin = value_of_key<T>(static_cast<Bits>(__ldg(vrange)), true);
+    const T vmax = value_of_key<T>(static_cast<Bits>(__ldg(vrange + 1)), true);
+    const T wlo = kPess ? vmin : -vmax, whi = kPess ? vmax : -vmin;
+    const T span = N::sub(whi, wlo);
+    const T bscale = span > T(0) ? T(B) / span : T(0);
+    auto bucket_of = [&](T val) -> int {
+        const T w = kPess ? val : -val;
+        int x = static_cast<int>(N::mul(N::sub(w, wlo), bscale));
+        x = x > 0 ? x : 0;
+        return x < B - 1 ? x : B - 1;
+    };
+    for (int i = t; i < 2 * B; i += NT) hbuf[i] = 0u;
+    if (t < 8) dwb[t] = 0;
+    __syncthreads();
+    unsigned par = 0;
 
     for (int item = blockIdx.x; item < nlist; item += gridDim.x) {
         const int c = __ldg(list + item);
         const long long b = __ldg(colptr + c);
         const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
         const T r = __ldg(rem + c);
-        // ---- load; sum V l; range of w ----
+        const bool picks = r > T(0);
+        unsigned* hist = hbuf + par * 2 * B;
+        unsigned* hcnt = hist + B;
+        int* dw = dwb + par * 4;
+        // ---- load (registers); sum V l; fixed-point gap histogram ----
         int rw[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int pos = e * NT + t;
             rw[e] = pos < L ? ld_hint(rows + b + pos, pstream) : 0;
         }
+        T v[E], g[E];
         T acc = T(0);
-        T wlo = T(0), whi = T(0);
-        bool any = false;
 #pragma unroll
         for (int h = 0; h < E; h += E / 2) { // two halves: 3 x E/2 loads in flight, fewer registers
-            T v[E / 2], g[E / 2], l[E / 2];
+            T l[E / 2];
 #pragma unroll
             for (int i = 0; i < E / 2; ++i) {
                 const int e = h + i, pos = e * NT + t;
+                v[e] = T(0);
+                g[e] = T(0);
+                l[i] = T(0);
                 if (pos < L) {
-                    v[i] = ld_hint(V + rw[e], pval);
-                    g[i] = ld_hint(gap + b + pos, pstream);
+                    v[e] = ld_hint(V + rw[e], pval);
+                    g[e] = ld_hint(gap + b + pos, pstream);
                     l[i] = ld_hint(lower + b + pos, pstream);
                 }
             }
 #pragma unroll
             for (int i = 0; i < E / 2; ++i) {
                 const int e = h + i, pos = e * NT + t;
-                if (pos < L) {
-                    acc = N::add(acc, N::mul(v[i], l[i]));
-                    const T w = kPess ? v[i] : -v[i];
-                    wlo = any ? (w < wlo ? w : wlo) : w;
-                    whi = any ? (w > whi ? w : whi) : w;
-                    any = true;
-                    sv[pos] = v[i];
-                    sgp[pos] = g[i];
-                }
+                if (pos < L) acc = N::add(acc, N::mul(v[e], l[i]));
             }
         }
-        for (int i = t; i < 2 * B; i += NT) hist[i] = 0u;
-        if (t < 4) dw[t] = 0;
-        if (!any) { // only threads past the end of a short column
-            wlo = T(1e300);
-            whi = T(-1e300);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const T a = __shfl_xor_sync(kFull, wlo, o), z = __shfl_xor_sync(kFull, whi, o);
-            wlo = a < wlo ? a : wlo;
-            whi = z > whi ? z : whi;
-        }
-        if (lane == 0) {
-            pa[wig] = wlo;
-            pb[wig] = whi;
-        }
-        __syncthreads();
-        wlo = pa[0];
-        whi = pb[0];
-#pragma unroll
-        for (int i = 1; i < NW; ++i) {
-            wlo = pa[i] < wlo ? pa[i] : wlo;
-            whi = pb[i] > whi ? pb[i] : whi;
-        }
-        const bool picks = r > T(0);
-        // ---- fixed-point gap histogram over the buckets ----
-        const T span = N::sub(whi, wlo);
-        const T bscale = span > T(0) ? T(B) / span : T(0);
         const T gm = __ldg(maxgap + c);
         const double sc = gm > T(0) ? 2147483648.0 / ((double)L * (double)gm) : 0.0;
-        auto bucket_of = [&](T val) -> int {
-            const T w = kPess ? val : -val;
-            const int x = static_cast<int>(N::mul(N::sub(w, wlo), bscale));
-            return x < B - 1 ? x : B - 1;
-        };
         if (picks) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                const int pos = e * NT + t;
-                if (pos < L) {
-                    const int bb = bucket_of(sv[pos]);
-                    atomicAdd(hist + bb, static_cast<unsigned>((double)sgp[pos] * sc));
+                if (e * NT + t < L) {
+                    const int bb = bucket_of(v[e]);
+                    atomicAdd(hist + bb, static_cast<unsigned>((double)g[e] * sc));
                     atomicAdd(hcnt + bb, 1u);
                 }
             }
         }
-        __syncthreads(); // also: partials pa / pb are free again
-        if (!picks) {
-            // no picks: q = sum V l
-        } else {
+        __syncthreads(); // B1: histogram complete
+        {   // the next column's buffers: their last readers (the previous column) are past B1
+            unsigned* oh = hbuf + (par ^ 1u) * 2 * B;
+            for (int i = t; i < 2 * B; i += NT) oh[i] = 0u;
+            if (t < 4) dwb[(par ^ 1u) * 4 + t] = 0;
+        }
+        T bs = T(0);
+        if (picks) {
             // ---- bracket of the cut's bucket: block-wide exclusive scan of the buckets ----
             constexpr int PB = B / NT > 0 ? B / NT : 1; // buckets per thread
             unsigned long long fm = 0, fn = 0;
@@ -1805,7 +1842,7 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                 wtot[wig] = em;
                 wtot[NW + wig] = en;
             }
-            __syncthreads();
+            __syncthreads(); // B2
             em -= fm;
             en -= fn;
             for (int i = 0; i < wig; ++i) {
@@ -1831,101 +1868,91 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                 if (blo >= 0) atomicMax(dw + 0, blo + 1);
                 if (bhi >= 0) atomicMax(dw + 1, bhi + 1);
             }
-            __syncthreads();
+            __syncthreads(); // B3
             const int blo = dw[0] > 0 ? dw[0] - 1 : 0; // the first entry is always reached (rem > 0)
             const int bhi = dw[1] - 1;
             // ---- entries before the bracket; candidates to shared memory ----
-            T bs = T(0);
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int pos = e * NT + t;
                 if (pos < L) {
-                    const T ve = sv[pos], ge = sgp[pos];
-                    const int bb = bucket_of(ve);
+                    const int bb = bucket_of(v[e]);
                     if (bb < blo) {
-                        bs = N::add(bs, ge);
-                        acc = N::add(acc, N::mul(ve, ge));
+                        bs = N::add(bs, g[e]);
+                        acc = N::add(acc, N::mul(v[e], g[e]));
                     } else if (bb <= bhi) {
                         const int slot = atomicAdd(dw + 3, 1);
                         if (slot < CAP) {
-                            ckey[slot] = static_cast<unsigned long long>(order_key<T>(ve, kPess));
-                            cg[slot] = ge;
-                            cv[slot] = ve;
+                            ckey[slot] = static_cast<unsigned long long>(order_key<T>(v[e], kPess));
+                            cg[slot] = g[e];
+                            cv[slot] = v[e];
                             cpos[slot] = pos;
                         }
                     }
                 }
             }
+        }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) bs = N::add(bs, __shfl_xor_sync(kFull, bs, o));
-            if (lane == 0) pa[wig] = bs;
-            __syncthreads();
-            const int K = dw[3];
-            if (K > CAP) {
-                // too many entries in the bracket (ties, clustered values): selection kernel
-                if (t == 0) fallback[atomicAdd(nfallback, 1)] = c;
-                __syncthreads(); // dw / hist / candidates stay stable until everyone has read them
-                continue;
+        for (int o = 16; o > 0; o >>= 1) {
+            bs = N::add(bs, __shfl_xor_sync(kFull, bs, o));
+            acc = N::add(acc, __shfl_xor_sync(kFull, acc, o));
+        }
+        if (lane == 0) {
+            pa[wig] = bs;
+            pb[wig] = acc;
+        }
+        __syncthreads(); // B4: partials and candidates complete
+        par ^= 1u;
+        const int K = picks ? dw[3] : 0;
+        if (K > CAP) {
+            // too many entries in the bracket (ties, clustered values): selection kernel
+            if (t == 0) fallback[atomicAdd(nfallback, 1)] = c;
+            continue;
+        }
+        if (wig != 0) continue;
+        // ---- warp 0: resolve the bracket, q ----
+        T add = T(0);
+        if (picks && K > 0) {
+            T base = pa[0];
+#pragma unroll
+            for (int i = 1; i < NW; ++i) base = N::add(base, pa[i]);
+            // two candidates per lane: index x = j * 32 + lane
+            unsigned long long kk[2];
+            int pp[2];
+            T gg[2], vv[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int x = j * 32 + lane;
+                const bool ok = x < K;
+                kk[j] = ok ? ckey[x] : ~0ull;
+                pp[j] = ok ? cpos[x] : INT_MAX;
+                gg[j] = ok ? cg[x] : T(0);
+                vv[j] = ok ? cv[x] : T(0);
             }
-            if (wig == 0 && K <= 32) {
-                // one candidate per lane: bitonic sort of 32 by (key, pos), prefix, cut
-                T base = pa[0];
-#pragma unroll
-                for (int i = 1; i < NW; ++i) base = N::add(base, pa[i]);
-                const bool ok = lane < K;
-                unsigned long long kk = ok ? ckey[lane] : ~0ull;
-                int pp = ok ? cpos[lane] : INT_MAX;
-                T gg = ok ? cg[lane] : T(0), vv = ok ? cv[lane] : T(0);
+            if (K <= 32) {
+                // one candidate per lane: bitonic sort of 32 by (key, pos)
 #pragma unroll
                 for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
                     for (int stride = size / 2; stride > 0; stride >>= 1) {
-                        const unsigned long long ok2 = __shfl_xor_sync(kFull, kk, stride);
-                        const int op = __shfl_xor_sync(kFull, pp, stride);
-                        const T og = __shfl_xor_sync(kFull, gg, stride);
-                        const T ov = __shfl_xor_sync(kFull, vv, stride);
+                        const unsigned long long ok2 = __shfl_xor_sync(kFull, kk[0], stride);
+                        const int op = __shfl_xor_sync(kFull, pp[0], stride);
+                        const T og = __shfl_xor_sync(kFull, gg[0], stride);
+                        const T ov = __shfl_xor_sync(kFull, vv[0], stride);
                         const bool lower_half = (lane & stride) == 0;
                         const bool up = (lane & size) == 0;
-                        const bool other_less = ok2 < kk || (ok2 == kk && op < pp);
+                        const bool other_less = ok2 < kk[0] || (ok2 == kk[0] && op < pp[0]);
                         if (lower_half == up ? other_less : !other_less) {
-                            kk = ok2;
-                            pp = op;
-                            gg = og;
-                            vv = ov;
+                            kk[0] = ok2;
+                            pp[0] = op;
+                            gg[0] = og;
+                            vv[0] = ov;
                         }
                     }
                 }
-                T inc = gg;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const T y = __shfl_up_sync(kFull, inc, o);
-                    if (lane >= o) inc = N::add(inc, y);
-                }
-                const T ex = N::add(base, N::sub(inc, gg));
-                const unsigned m0 = __ballot_sync(kFull, ok && ex < r);
-                const int cx = m0 ? 31 - __clz(m0) : -1;
-                if (lane < cx) acc = N::add(acc, N::mul(vv, gg));
-                else if (lane == cx) {
-                    const T avail = N::sub(r, ex);
-                    acc = N::add(acc, N::mul(vv, gg < avail ? gg : avail));
-                }
-            } else if (wig == 0) {
-                T base = pa[0];
-#pragma unroll
-                for (int i = 1; i < NW; ++i) base = N::add(base, pa[i]);
-                // two candidates per lane: index x = j * 32 + lane
-                unsigned long long kk[2];
-                int pp[2];
-                T gg[2], vv[2];
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const int x = j * 32 + lane;
-                    const bool ok = x < K;
-                    kk[j] = ok ? ckey[x] : ~0ull;
-                    pp[j] = ok ? cpos[x] : INT_MAX;
-                    gg[j] = ok ? cg[x] : T(0);
-                    vv[j] = ok ? cv[x] : T(0);
-                }
+                gg[1] = T(0);
+                vv[1] = T(0);
+            } else {
                 // bitonic sort of 64 by (key, pos) ascending
 #pragma unroll
                 for (int size = 2; size <= 64; size <<= 1) {
@@ -1964,51 +1991,45 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                         }
                     }
                 }
-                // exclusive prefix of the gaps in sorted order (x = j * 32 + lane)
-                T ex[2];
-                T tot0 = T(0);
+            }
+            // exclusive prefix of the gaps in sorted order (x = j * 32 + lane)
+            T ex[2];
+            T tot0 = T(0);
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    T inc = gg[j];
+            for (int j = 0; j < 2; ++j) {
+                T inc = gg[j];
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const T y = __shfl_up_sync(kFull, inc, o);
-                        if (lane >= o) inc = N::add(inc, y);
-                    }
-                    ex[j] = N::sub(inc, gg[j]);
-                    if (j == 0) tot0 = __shfl_sync(kFull, inc, 31);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const T y = __shfl_up_sync(kFull, inc, o);
+                    if (lane >= o) inc = N::add(inc, y);
                 }
-                ex[0] = N::add(base, ex[0]);
-                ex[1] = N::add(N::add(base, tot0), ex[1]);
-                // the cut: last candidate (in order) whose prefix is < rem
-                const bool r0 = lane < K && ex[0] < r, r1 = 32 + lane < K && ex[1] < r;
-                const unsigned m0 = __ballot_sync(kFull, r0), m1 = __ballot_sync(kFull, r1);
-                const int cx = m1 ? 32 + 31 - __clz(m1) : (m0 ? 31 - __clz(m0) : -1);
-                T add = T(0);
+                ex[j] = N::sub(inc, gg[j]);
+                if (j == 0) tot0 = __shfl_sync(kFull, inc, 31);
+            }
+            ex[0] = N::add(base, ex[0]);
+            ex[1] = N::add(N::add(base, tot0), ex[1]);
+            // the cut: last candidate (in order) whose prefix is < rem
+            const bool r0 = lane < K && ex[0] < r, r1 = 32 + lane < K && ex[1] < r;
+            const unsigned m0 = __ballot_sync(kFull, r0), m1 = __ballot_sync(kFull, r1);
+            const int cx = m1 ? 32 + 31 - __clz(m1) : (m0 ? 31 - __clz(m0) : -1);
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const int x = j * 32 + lane;
-                    if (x < cx) add = N::add(add, N::mul(vv[j], gg[j]));
-                    else if (x == cx) {
-                        const T avail = N::sub(r, ex[j]);
-                        add = N::add(add, N::mul(vv[j], gg[j] < avail ? gg[j] : avail));
-                    }
+            for (int j = 0; j < 2; ++j) {
+                const int x = j * 32 + lane;
+                if (x < cx) add = N::add(add, N::mul(vv[j], gg[j]));
+                else if (x == cx) {
+                    const T avail = N::sub(r, ex[j]);
+                    add = N::add(add, N::mul(vv[j], gg[j] < avail ? gg[j] : avail));
                 }
-                acc = N::add(acc, add);
             }
         }
-        // ---- q = sum over the CTA ----
+        // ---- q = sum of the warps' partials + the bracket's share ----
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc = N::add(acc, __shfl_xor_sync(kFull, acc, o));
-        __syncthreads();
-        if (lane == 0) pb[wig] = acc;
-        __syncthreads();
-        if (t == 0) {
+        for (int o = 16; o > 0; o >>= 1) add = N::add(add, __shfl_xor_sync(kFull, add, o));
+        if (lane == 0) {
             T s2 = pb[0];
             for (int i = 1; i < NW; ++i) s2 = N::add(s2, pb[i]);
-            q[c] = s2;
+            q[c] = N::add(s2, add);
         }
-        __syncthreads();
     }
 }
 
