@@ -698,6 +698,28 @@ void launch_select_class(rimdp_model* m, int count, const int* list, const T* V,
                                               count_dev);
 }
 
+// Fallback list of one size class: [count A, count B, columns...].  The
+// bucket kernels count into one counter and clear the other, alternating
+// between launches, so no memset sits between the kernels of an iteration.
+struct FallbackSlots {
+    int* list;
+    int* count;
+    int* other;
+};
+
+FallbackSlots fallback_slots(rimdp_model* m, int cls, int count) {
+    DevBuf& fbuf = m->fallback[cls];
+    const size_t need = sizeof(int) * (size_t)(std::max(count, 1) + 2);
+    if (fbuf.bytes < need) {
+        fbuf.ensure(need);
+        CK(cudaMemsetAsync(fbuf.p, 0, 2 * sizeof(int), m->ls));
+    }
+    int& par = m->fallback_parity[cls];
+    FallbackSlots f{fbuf.as<int>() + 2, fbuf.as<int>() + par, fbuf.as<int>() + (par ^ 1)};
+    par ^= 1;
+    return f;
+}
+
 // Columns of more than 256 entries: value-bucket kernel, then the selection
 // kernel over the columns it could not bracket tightly (fallback list).
 template <class T, bool P, int LG>
@@ -714,23 +736,32 @@ void launch_bucket_class(rimdp_model* m, int count, const DevBuf& list, const T*
         per_sm[dev] = std::max(per_sm[dev], 1);
         configured[dev] = true;
     }
-    DevBuf& fbuf = m->fallback[LG - kSortedMinLog];
-    const size_t need = sizeof(int) * (size_t)(std::max(count, 1) + 2);
-    if (fbuf.bytes < need) {
-        fbuf.ensure(need);
-        CK(cudaMemsetAsync(fbuf.p, 0, 2 * sizeof(int), m->ls));
-    }
-    // [count A, count B, columns...]: launches alternate between the two counters
-    int& par = m->fallback_parity[LG - kSortedMinLog];
-    int* nfb = fbuf.as<int>() + par;
-    int* other = fbuf.as<int>() + (par ^ 1);
-    par ^= 1;
-    int* fb = fbuf.as<int>() + 2;
+    const FallbackSlots f = fallback_slots(m, LG - kSortedMinLog, count);
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
-    launch_pdl(m->pdl_now, k, blocks, Sh::NT, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
-                                           m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V,
-                                           q, ctl, fb, nfb, other, m->vrange_cur);
-    launch_select_class<T, P, LG>(m, count, fb, V, q, ctl, nfb);
+    launch_pdl(m->pdl_now, k, blocks, Sh::NT, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
+               m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V, q, ctl,
+               f.list, f.count, f.other, m->vrange_cur);
+    launch_select_class<T, P, LG>(m, count, f.list, V, q, ctl, f.count);
+}
+
+// Many-pick columns of 33 .. 256 entries: warp-per-column value buckets,
+// then the selection kernel over the fallback list.
+template <class T, bool P, int LG>
+void launch_wbucket_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
+    using Sh = WBucketShape<LG>;
+    auto k = omax_wbucket<T, P, LG>;
+    static int per_sm[64] = {};
+    const int dev = m->device & 63;
+    if (!per_sm[dev]) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, Sh::W * 32, 0));
+        per_sm[dev] = std::max(per_sm[dev], 1);
+    }
+    const FallbackSlots f = fallback_slots(m, LG - kSortedMinLog, count);
+    const int blocks = grid_for(count, Sh::W, m->sm_count, per_sm[dev]);
+    launch_pdl(m->pdl_now, k, blocks, Sh::W * 32, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
+               m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V, q, ctl,
+               f.list, f.count, f.other, m->vrange_cur);
+    launch_select_class<T, P, LG>(m, count, f.list, V, q, ctl, f.count);
 }
 
 // Many-pick long columns by size class: weighted quickselect (omax_select,
@@ -744,6 +775,8 @@ void launch_sorted(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* 
                 launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else if (LG >= 9 && m->bucket)
                 launch_bucket_class<T, P, (LG >= 9 ? LG : 9)>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+            else if (LG <= 8 && m->bucket)
+                launch_wbucket_class<T, P, (LG <= 8 ? LG : 8)>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else
                 launch_select_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i].as<int>(), V, q, ctl);
         }
@@ -897,6 +930,8 @@ void launch_sorted_fanout(rimdp_model* m, const ColumnLists& L, const T* V, T* q
                 launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else if (LG >= 9 && m->bucket)
                 launch_bucket_class<T, P, (LG >= 9 ? LG : 9)>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+            else if (LG <= 8 && m->bucket)
+                launch_wbucket_class<T, P, (LG <= 8 ? LG : 8)>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else
                 launch_select_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i].as<int>(), V, q, ctl);
         }
@@ -910,7 +945,7 @@ void launch_sorted_fanout(rimdp_model* m, const ColumnLists& L, const T* V, T* q
 template <class T>
 void launch_value_range(rimdp_model* m, const ColumnLists& L, const T* V) {
     bool need = false;
-    for (int i = 9 - kSortedMinLog; i < kSortedClasses; ++i) need = need || L.n_sorted[i] > 0;
+    for (int i = 0; i < kSortedClasses; ++i) need = need || L.n_sorted[i] > 0;
     m->vrange_cur = nullptr;
     if (!need || m->bitonic || !m->bucket) return;
     if (!m->vrange.p) {

@@ -2033,6 +2033,200 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
     }
 }
 
+// Many-pick columns of 33 .. 256 entries: omax_bucket's method at warp
+// scale.  One warp per column, E = Len / 32 entries per lane in registers,
+// B = Len / 4 value buckets over the value vector's range (value_range), a
+// fixed-point gap histogram in the warp's shared memory, a warp scan for the
+// bracket [b_lo, b_hi], no block barriers.  The bracket's entries (<= 32)
+// are compacted one per lane in position order (ballot ranks) and resolved by
+// the greedy itself (omax.hpp:98-112): exact warp argmins over their order
+// keys, `consumed` continued sequentially from the exact base (the gaps
+// below the bracket, tree order), so only the few picks inside the bracket
+// are walked.  A bracket of more than 32 entries goes to the fallback list
+// (omax_select).  Tree-order sums: within a few ulps of the reference.
+template <int LG>
+struct WBucketShape {
+    static constexpr int Len = 1 << LG;
+    static constexpr int E = Len / 32;          // 2, 4, 8
+    static constexpr int B = Len / 4;           // 16, 32, 64
+    static constexpr int PB = B >= 32 ? B / 32 : 1;
+    static constexpr int W = 8;                 // warps per block
+    static constexpr int WarpBytes = 2 * 4 * B + 32 * (8 + 2 * 8);
+};
+
+template <class T, bool kPess, int LG>
+__global__ void __launch_bounds__(WBucketShape<LG>::W * 32)
+omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+             const T* __restrict__ rem, const T* __restrict__ maxgap, const T* __restrict__ V, T* __restrict__ q,
+             const Ctl* __restrict__ ctl, int* __restrict__ fallback, int* __restrict__ nfallback,
+             int* __restrict__ other_nfallback, const unsigned long long* __restrict__ vrange) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    using Sh = WBucketShape<LG>;
+    constexpr int E = Sh::E, B = Sh::B, PB = Sh::PB, W = Sh::W;
+    pdl_enter();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *other_nfallback = 0;
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    __shared__ __align__(16) unsigned char smem[W * Sh::WarpBytes];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned* hist = reinterpret_cast<unsigned*>(smem + w * Sh::WarpBytes);
+    unsigned* hcnt = hist + B;
+    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hcnt + B);
+    T* cg = reinterpret_cast<T*>(ckey + 32);
+    T* cv = cg + 32;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
+    const T vmin = value_of_key<T>(static_cast<Bits>(__ldg(vrange)), true);
+    const T vmax = value_of_key<T>(static_cast<Bits>(__ldg(vrange + 1)), true);
+    const T wlo = kPess ? vmin : -vmax, whi = kPess ? vmax : -vmin;
+    const T span = N::sub(whi, wlo);
+    const T bscale = span > T(0) ? T(B) / span : T(0);
+    auto bucket_of = [&](T val) -> int {
+        const T wv = kPess ? val : -val;
+        int x = static_cast<int>(N::mul(N::sub(wv, wlo), bscale));
+        x = x > 0 ? x : 0;
+        return x < B - 1 ? x : B - 1;
+    };
+    const int gw = blockIdx.x * W + w, nw = gridDim.x * W;
+    for (int item = gw; item < nlist; item += nw) {
+        const int c = __ldg(list + item);
+        const long long b = __ldg(colptr + c);
+        const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
+        const T r = __ldg(rem + c);
+        const bool picks = r > T(0);
+        int rw[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = e * 32 + lane;
+            rw[e] = pos < L ? ld_hint(rows + b + pos, pstream) : 0;
+        }
+        T v[E], g[E];
+        T acc = T(0);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = e * 32 + lane;
+            v[e] = T(0);
+            g[e] = T(0);
+            if (pos < L) {
+                v[e] = ld_hint(V + rw[e], pval);
+                g[e] = ld_hint(gap + b + pos, pstream);
+                acc = N::add(acc, N::mul(v[e], ld_hint(lower + b + pos, pstream)));
+            }
+        }
+        T add = T(0);
+        if (picks) {
+            // ---- fixed-point gap histogram (warp-private) ----
+#pragma unroll
+            for (int i = lane; i < 2 * B; i += 32) hist[i] = 0u;
+            __syncwarp();
+            const T gm = __ldg(maxgap + c);
+            const double sc = gm > T(0) ? 2147483648.0 / ((double)L * (double)gm) : 0.0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (e * 32 + lane < L) {
+                    const int bb = bucket_of(v[e]);
+                    atomicAdd(hist + bb, static_cast<unsigned>((double)g[e] * sc));
+                    atomicAdd(hcnt + bb, 1u);
+                }
+            }
+            __syncwarp();
+            // ---- bracket: warp scan of the buckets (lane owns PB consecutive buckets) ----
+            unsigned fm = 0, fn = 0;
+#pragma unroll
+            for (int i = 0; i < PB; ++i) {
+                const int bb = lane * PB + i;
+                if (bb < B) {
+                    fm += hist[bb];
+                    fn += hcnt[bb];
+                }
+            }
+            unsigned em = fm, en = fn;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned a = __shfl_up_sync(kFull, em, o), z = __shfl_up_sync(kFull, en, o);
+                if (lane >= o) {
+                    em += a;
+                    en += z;
+                }
+            }
+            em -= fm;
+            en -= fn;
+            const double R = (double)r * sc;
+            int blo = -1, bhi = -1;
+#pragma unroll
+            for (int i = 0; i < PB; ++i) {
+                const int bb = lane * PB + i;
+                if (bb < B) {
+                    const unsigned hm = hist[bb], hn = hcnt[bb];
+                    if (hn > 0) {
+                        if ((double)em + (double)en <= R) blo = bb;
+                        if ((double)em < R) bhi = bb;
+                    }
+                    em += hm;
+                    en += hn;
+                }
+            }
+            const int lo_b = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(blo + 1)));
+            const int hi_b = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(bhi + 1))) - 1;
+            const int bl = lo_b > 0 ? lo_b - 1 : 0; // the first entry is always reached (rem > 0)
+            // ---- below the bracket: exact base; the bracket: compacted one per lane ----
+            T bs = T(0);
+            int K = 0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int pos = e * 32 + lane;
+                const int bb = pos < L ? bucket_of(v[e]) : B;
+                if (bb < bl) {
+                    bs = N::add(bs, g[e]);
+                    acc = N::add(acc, N::mul(v[e], g[e]));
+                }
+                const bool in = bb >= bl && bb <= hi_b;
+                const unsigned m = __ballot_sync(kFull, in);
+                const int slot = K + __popc(m & lt);
+                if (in && slot < 32) {
+                    ckey[slot] = static_cast<unsigned long long>(order_key<T>(v[e], kPess));
+                    cg[slot] = g[e];
+                    cv[slot] = v[e];
+                }
+                K += __popc(m);
+            }
+            if (K > 32) {
+                // too many entries in the bracket (ties, clustered values): selection kernel
+                if (lane == 0) fallback[atomicAdd(nfallback, 1)] = c;
+                __syncwarp();
+                continue;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) bs = N::add(bs, __shfl_xor_sync(kFull, bs, o));
+            __syncwarp();
+            // ---- the greedy inside the bracket (slot order = position order) ----
+            const bool ok = lane < K;
+            Bits key = ok ? static_cast<Bits>(ckey[lane]) : ~Bits(0);
+            const T gl = ok ? cg[lane] : T(0), vl = ok ? cv[lane] : T(0);
+            T consumed = bs;
+            T avail = N::sub(r, consumed);
+            for (int nsel = 0; avail > T(0) && nsel < K; ++nsel) {
+                const int sel = warp_argmin_sentinel(key);
+                const T gs = __shfl_sync(kFull, gl, sel);
+                if (lane == sel) {
+                    add = N::mul(vl, gl < avail ? gl : avail);
+                    key = ~Bits(0);
+                }
+                consumed = N::add(consumed, gs);
+                avail = N::sub(r, consumed);
+            }
+            __syncwarp(); // candidates and histogram are rewritten by the next column
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            acc = N::add(acc, __shfl_xor_sync(kFull, acc, o));
+            add = N::add(add, __shfl_xor_sync(kFull, add, o));
+        }
+        if (lane == 0) q[c] = N::add(acc, add);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Action reduction + reach/avoid/discount update + residual + stop test
 // (bellman.hpp:88-115, solver.hpp:107-134).  Each block folds its max of

@@ -102,6 +102,24 @@ def test_select_random_values_within_tolerance(powerlaw, pess):
 
 
 @pytest.mark.parametrize("pess", [True, False])
+def test_default_random_values_within_tolerance(powerlaw, pess):
+    """Default routing (value buckets: omax_bucket for > 256 entries,
+    omax_wbucket for 33-256) on continuous values, f64 and f32; deterministic."""
+    v = np.random.default_rng(9).random(9000)
+    ref = ref_columns(powerlaw, v, pess)
+    m = engine.DeviceModel.from_csc(*powerlaw)
+    q = m.column_values(v, pess)
+    assert np.abs(q - ref).max() <= COL_TOL
+    assert np.array_equal(bits(q), bits(m.column_values(v, pess)))
+    sp, cp, rv, lo, up = powerlaw
+    arr32 = (sp, cp, rv, lo.astype(np.float32), up.astype(np.float32))
+    v32 = v.astype(np.float32)
+    ref32 = ref_columns(arr32, v32, pess)
+    q32 = engine.DeviceModel.from_csc(*arr32).column_values(v32, pess)
+    assert np.abs(q32.astype(np.float64) - ref32).max() <= 1e-5
+
+
+@pytest.mark.parametrize("pess", [True, False])
 def test_exact_long_kernel_bit_exact(powerlaw, pess):
     v = tricky_values(9000, 4)
     ref = ref_columns(powerlaw, v, pess)
