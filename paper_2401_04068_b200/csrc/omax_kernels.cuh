@@ -195,11 +195,15 @@ __device__ __forceinline__ typename Num<T>::Bits order_key(T v, bool pess) {
 }
 
 // Lane with the smallest (key, lane); inactive lanes carry the all-ones key.
+// The high word usually decides alone (one lane holds the minimum high
+// word): then the second redux is skipped (warp-uniform branch).
 template <class Bits>
 __device__ __forceinline__ int warp_argmin_sentinel(Bits key) {
     if constexpr (sizeof(Bits) == 8) {
         const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
         const unsigned mhi = __reduce_min_sync(kFull, hi);
+        const unsigned wh = __ballot_sync(kFull, hi == mhi);
+        if ((wh & (wh - 1u)) == 0u) return __ffs(wh) - 1;
         const unsigned mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xffffffffu);
         return __ffs(__ballot_sync(kFull, hi == mhi && lo == mlo)) - 1;
     } else {
