@@ -154,7 +154,8 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm), "samples_in_timed_region": inside,
-                "window": "timed region through kernel-timing pass and end-to-end solve (GPU busy)"}
+                "window": "timed region through the kernel-timing pass (GPU busy); stopped before the "
+                          "end-to-end solve"}
 
 
 # ---------------------------------------------------------------------------
@@ -330,6 +331,9 @@ def engine_arm(args, w):
             traffic = json.load(f).get(f"{args.config}_{args.dtype}", {}).get("dram_bytes_per_launch")
 
     # ---- end to end through the public API with host buffers ------------
+    # the clock sampler stops first: nvidia-smi's NVML queries contend with
+    # the driver calls of the upload (measured: occasional 50 ms stalls)
+    clk.__exit__()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -373,7 +377,6 @@ def engine_arm(args, w):
             idx = np.array(run["sample_idx"])
             sample_diff = float(np.abs(values[idx] - np.array([float.fromhex(h) for h in run["sample_hex"]])).max())
     m.close()
-    clk.__exit__()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample(w, dtype, budget_s=args.cpu_budget)
