@@ -120,6 +120,26 @@ def test_default_random_values_within_tolerance(powerlaw, pess):
 
 
 @pytest.mark.parametrize("pess", [True, False])
+@pytest.mark.parametrize("values", ["constant", "outlier", "negative"])
+def test_value_buckets_degenerate_ranges(powerlaw, pess, values):
+    """The value buckets span the whole vector's range: a constant vector (zero
+    span: one bucket), one huge outlier (every other value in the first
+    bucket) and negative values must still give the reference's columns
+    (brackets too wide go to the selection fallback)."""
+    rng = np.random.default_rng(12)
+    if values == "constant":
+        v = np.full(9000, 0.375)
+    elif values == "outlier":
+        v = rng.random(9000)
+        v[17] = 1e6
+    else:
+        v = rng.random(9000) - 0.5
+    ref = ref_columns(powerlaw, v, pess)
+    q = engine.DeviceModel.from_csc(*powerlaw).column_values(v, pess)
+    assert np.abs(q - ref).max() <= COL_TOL * max(1.0, np.abs(v).max())
+
+
+@pytest.mark.parametrize("pess", [True, False])
 def test_exact_long_kernel_bit_exact(powerlaw, pess):
     v = tricky_values(9000, 4)
     ref = ref_columns(powerlaw, v, pess)
