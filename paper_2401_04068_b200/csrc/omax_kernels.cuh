@@ -1914,121 +1914,50 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             continue;
         }
         if (wig != 0) continue;
-        // ---- warp 0: resolve the bracket, q ----
+        // ---- warp 0: the greedy (omax.hpp:98-112) inside the bracket, q ----
+        // Two candidates per lane (slots lane, 32 + lane).  `consumed` starts
+        // at the exact base below the bracket and grows along the adversary
+        // order: each pick is the exact warp argmin over (order key, position),
+        // so only the picks up to the cut are walked (typically a handful).
+        // The picks' shares are summed in pick order, so q does not depend on
+        // which slot a candidate landed in.
         T add = T(0);
         if (picks && K > 0) {
             T base = pa[0];
 #pragma unroll
             for (int i = 1; i < NW; ++i) base = N::add(base, pa[i]);
-            // two candidates per lane: index x = j * 32 + lane
-            unsigned long long kk[2];
-            int pp[2];
-            T gg[2], vv[2];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int x = j * 32 + lane;
-                const bool ok = x < K;
-                kk[j] = ok ? ckey[x] : ~0ull;
-                pp[j] = ok ? cpos[x] : INT_MAX;
-                gg[j] = ok ? cg[x] : T(0);
-                vv[j] = ok ? cv[x] : T(0);
-            }
-            if (K <= 32) {
-                // one candidate per lane: bitonic sort of 32 by (key, pos)
-#pragma unroll
-                for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-                    for (int stride = size / 2; stride > 0; stride >>= 1) {
-                        const unsigned long long ok2 = __shfl_xor_sync(kFull, kk[0], stride);
-                        const int op = __shfl_xor_sync(kFull, pp[0], stride);
-                        const T og = __shfl_xor_sync(kFull, gg[0], stride);
-                        const T ov = __shfl_xor_sync(kFull, vv[0], stride);
-                        const bool lower_half = (lane & stride) == 0;
-                        const bool up = (lane & size) == 0;
-                        const bool other_less = ok2 < kk[0] || (ok2 == kk[0] && op < pp[0]);
-                        if (lower_half == up ? other_less : !other_less) {
-                            kk[0] = ok2;
-                            pp[0] = op;
-                            gg[0] = og;
-                            vv[0] = ov;
-                        }
-                    }
+            unsigned long long k0 = lane < K ? ckey[lane] : ~0ull;
+            unsigned long long k1 = 32 + lane < K ? ckey[32 + lane] : ~0ull;
+            const int p0 = lane < K ? cpos[lane] : INT_MAX, p1 = 32 + lane < K ? cpos[32 + lane] : INT_MAX;
+            const T g0 = lane < K ? cg[lane] : T(0), g1 = 32 + lane < K ? cg[32 + lane] : T(0);
+            const T v0 = lane < K ? cv[lane] : T(0), v1 = 32 + lane < K ? cv[32 + lane] : T(0);
+            T consumed = base;
+            T avail = N::sub(r, consumed);
+            for (int nsel = 0; avail > T(0) && nsel < K; ++nsel) {
+                const bool first = k0 < k1 || (k0 == k1 && p0 < p1);
+                const unsigned long long lk = first ? k0 : k1;
+                const int lp = first ? p0 : p1;
+                const unsigned hi = static_cast<unsigned>(lk >> 32), lo = static_cast<unsigned>(lk);
+                const unsigned mhi = __reduce_min_sync(kFull, hi);
+                bool cand = hi == mhi;
+                const unsigned mlo = __reduce_min_sync(kFull, cand ? lo : 0xffffffffu);
+                cand = cand && lo == mlo;
+                const unsigned mp = __reduce_min_sync(kFull, cand ? static_cast<unsigned>(lp) : 0xffffffffu);
+                cand = cand && static_cast<unsigned>(lp) == mp;
+                const int sel = __ffs(__ballot_sync(kFull, cand)) - 1;
+                const T gl = first ? g0 : g1, vl = first ? v0 : v1;
+                const T gs = __shfl_sync(kFull, gl, sel);
+                // the share of the pick, summed in pick order (candidate slots are not deterministic)
+                add = N::add(add, __shfl_sync(kFull, N::mul(vl, gl < avail ? gl : avail), sel));
+                if (lane == sel) {
+                    if (first) k0 = ~0ull;
+                    else k1 = ~0ull;
                 }
-                gg[1] = T(0);
-                vv[1] = T(0);
-            } else {
-                // bitonic sort of 64 by (key, pos) ascending
-#pragma unroll
-                for (int size = 2; size <= 64; size <<= 1) {
-#pragma unroll
-                    for (int stride = size / 2; stride > 0; stride >>= 1) {
-                        if (stride == 32) {
-                            // partner in the same lane (j = 0 <-> 1); ascending iff (x & size) == 0
-                            const bool up = (lane & size) == 0; // size == 64: always up
-                            const bool gt = kk[0] > kk[1] || (kk[0] == kk[1] && pp[0] > pp[1]);
-                            if (gt == up) {
-                                const unsigned long long a = kk[0]; kk[0] = kk[1]; kk[1] = a;
-                                const int bp = pp[0]; pp[0] = pp[1]; pp[1] = bp;
-                                const T cgx = gg[0]; gg[0] = gg[1]; gg[1] = cgx;
-                                const T cvx = vv[0]; vv[0] = vv[1]; vv[1] = cvx;
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 2; ++j) {
-                                const int x = j * 32 + lane;
-                                const unsigned long long ok2 = __shfl_xor_sync(kFull, kk[j], stride);
-                                const int op = __shfl_xor_sync(kFull, pp[j], stride);
-                                const T og = __shfl_xor_sync(kFull, gg[j], stride);
-                                const T ov = __shfl_xor_sync(kFull, vv[j], stride);
-                                const bool lower_half = (x & stride) == 0;
-                                const bool up = (x & size) == 0;
-                                // the lower index keeps the smaller when ascending
-                                const bool other_less = ok2 < kk[j] || (ok2 == kk[j] && op < pp[j]);
-                                const bool take = lower_half == up ? other_less : !other_less;
-                                if (take) {
-                                    kk[j] = ok2;
-                                    pp[j] = op;
-                                    gg[j] = og;
-                                    vv[j] = ov;
-                                }
-                            }
-                        }
-                    }
-                }
-            }
-            // exclusive prefix of the gaps in sorted order (x = j * 32 + lane)
-            T ex[2];
-            T tot0 = T(0);
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                T inc = gg[j];
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const T y = __shfl_up_sync(kFull, inc, o);
-                    if (lane >= o) inc = N::add(inc, y);
-                }
-                ex[j] = N::sub(inc, gg[j]);
-                if (j == 0) tot0 = __shfl_sync(kFull, inc, 31);
-            }
-            ex[0] = N::add(base, ex[0]);
-            ex[1] = N::add(N::add(base, tot0), ex[1]);
-            // the cut: last candidate (in order) whose prefix is < rem
-            const bool r0 = lane < K && ex[0] < r, r1 = 32 + lane < K && ex[1] < r;
-            const unsigned m0 = __ballot_sync(kFull, r0), m1 = __ballot_sync(kFull, r1);
-            const int cx = m1 ? 32 + 31 - __clz(m1) : (m0 ? 31 - __clz(m0) : -1);
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int x = j * 32 + lane;
-                if (x < cx) add = N::add(add, N::mul(vv[j], gg[j]));
-                else if (x == cx) {
-                    const T avail = N::sub(r, ex[j]);
-                    add = N::add(add, N::mul(vv[j], gg[j] < avail ? gg[j] : avail));
-                }
+                consumed = N::add(consumed, gs);
+                avail = N::sub(r, consumed);
             }
         }
-        // ---- q = sum of the warps' partials + the bracket's share ----
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) add = N::add(add, __shfl_xor_sync(kFull, add, o));
+        // ---- q = sum of the warps' partials + the bracket's share (warp-uniform) ----
         if (lane == 0) {
             T s2 = pb[0];
             for (int i = 1; i < NW; ++i) s2 = N::add(s2, pb[i]);
