@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -63,18 +64,59 @@ int fail(int status, const char* fmt, ...) {
 
 size_t elem_size(rimdp_dtype t) { return t == RIMDP_F64 ? 8 : 4; }
 
+// Device memory comes from the device's default stream-ordered pool with an
+// unlimited release threshold: memory a destroyed model gives back stays
+// mapped in the pool and serves the next model's allocations without driver
+// calls (cudaMalloc of fresh pages measured 1-14 ms per model and up to
+// 330 ms on a fresh box; model destroy 26 ms with cudaFree).
+void* dev_alloc(size_t b) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    {
+        static std::mutex mu;
+        static bool configured[64] = {};
+        std::lock_guard<std::mutex> lk(mu);
+        if (!configured[dev & 63]) {
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+            unsigned long long thr = ~0ull;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+            configured[dev & 63] = true;
+        }
+    }
+    void* p = nullptr;
+    CK(cudaMallocAsync(&p, b, 0));
+    CK(cudaStreamSynchronize(0)); // usable from every stream from here on
+    return p;
+}
+
+// Returns an allocation to the pool once every stream of its device is idle
+// (the memory may still be in use by queued work on any of them).
+void dev_free(void* p, int dev) {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != dev) cudaSetDevice(dev);
+    cudaDeviceSynchronize();
+    cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
+    if (cur >= 0 && cur != dev) cudaSetDevice(cur);
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
-    ~DevBuf() {
-        if (p) cudaFree(p);
+    int dev = 0;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) dev_free(p, dev);
+        p = nullptr;
+        bytes = 0;
     }
     void ensure(size_t b) {
         if (b <= bytes) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-        CK(cudaMalloc(&p, b > 0 ? b : 16));
+        release();
+        CK(cudaGetDevice(&dev));
+        p = dev_alloc(b > 0 ? b : 16);
         bytes = b;
     }
     template <class U>
@@ -335,6 +377,33 @@ void launch_pdl(bool on, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t
     CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+// RIMDP_TRACE=1: host-side phase times of model upload and solve on stderr.
+struct PhaseTrace {
+    const char* what;
+    bool on;
+    std::chrono::steady_clock::time_point t0, last;
+    explicit PhaseTrace(const char* w) : what(w) {
+        static const bool env_on = [] {
+            const char* e = getenv("RIMDP_TRACE");
+            return e && atoi(e) != 0;
+        }();
+        on = env_on;
+        t0 = last = std::chrono::steady_clock::now();
+    }
+    void mark(const char* phase) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[rimdp] %s %s %.2f ms\n", what, phase,
+                std::chrono::duration<double, std::milli>(t - last).count());
+        last = t;
+    }
+    ~PhaseTrace() {
+        if (on)
+            fprintf(stderr, "[rimdp] %s total %.2f ms\n", what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 int grid_for(long long work, int per_block, int sm_count, int blocks_per_sm) {
     long long g = (work + per_block - 1) / per_block;
     g = std::min<long long>(g, (long long)sm_count * blocks_per_sm);
@@ -426,12 +495,14 @@ void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, co
 //    remaining states take the q path (column kernels + action_reduce).
 template <class T>
 void build_schedule(rimdp_model* m, const long long* h_colptr) {
+    PhaseTrace tr("schedule");
     std::vector<T> h_rem(m->ncols), h_maxgap(m->ncols);
     if (m->ncols > 0) {
         CK(cudaMemcpyAsync(h_rem.data(), m->rem.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
         CK(cudaMemcpyAsync(h_maxgap.data(), m->maxgap.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
         CK(cudaStreamSynchronize(m->stream));
     }
+    tr.mark("d2h");
     const int mode = long_mode();
     m->bitonic = mode == 2;
     m->long_exact = mode == 1;
@@ -487,9 +558,11 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         bstates.back().y += 1;
     }
     close_batch();
+    tr.mark("classify");
     m->maxlen = maxlen;
     fill_lists(m, m->all, allc, cls);
     fill_lists(m, m->qp, qc, cls);
+    tr.mark("lists");
     m->nbatch = (int)bstates.size();
     m->nlong_states = (int)lstates.size();
     upload_list(m, m->batch_slots, slots);
@@ -1187,10 +1260,8 @@ void prepare_chosen(rimdp_model* m, const rimdp_outputs* o, const rimdp_plan* p)
         s.chosen.ensure(sizeof(int) * (size_t)m->n * rows);
         CK(cudaMemsetAsync(s.chosen.p, 0xff, sizeof(int) * (size_t)m->n * rows, m->stream));
     } else if (s.chosen.p) {
-        // keep the allocation but do not record
-        cudaFree(s.chosen.p);
-        s.chosen.p = nullptr;
-        s.chosen.bytes = 0;
+        // do not record
+        s.chosen.release();
     }
 }
 
@@ -1200,9 +1271,11 @@ int solve_t(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
     if (will_step) {
         if (const Infeasible* f = first_evaluated_infeasible(m, p)) return report_infeasible(f, m->dtype);
     }
+    PhaseTrace tr("solve");
     m->s.record_only = false;
     upload_plan<T>(m, p);
     prepare_chosen(m, o, p);
+    tr.mark("plan");
     const long long total = p->finite ? p->horizon : p->max_iterations;
     long long k = 0;
     Ctl c{};
@@ -1225,8 +1298,10 @@ int solve_t(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
         }
         k = c.k;
     }
+    tr.mark("iterations");
     if (c.status == 2) return fail(RIMDP_ERR_INTERNAL, "partial-assignment overflow in a long column");
     finish_t<T>(m, o, k);
+    tr.mark("finish");
     m->s.active = false;
     if (c.status == 1) {
         fail(RIMDP_ERR_NON_CONVERGENCE, "no convergence after %lld iterations (max residual %f)", k, c.res_last);
@@ -1340,9 +1415,11 @@ static int model_create_impl(const rimdp_model_desc* d, int state_begin, int num
         for (int s = 0; s < d->num_states; ++s)
             if (d->stateptr[s + 1] < d->stateptr[s])
                 return fail(RIMDP_ERR_INVALID_ARGUMENT, "stateptr not monotone at %d", s);
+        PhaseTrace tr("model_create");
         std::unique_ptr<rimdp_model> m(new rimdp_model);
         m->dtype = d->dtype;
         init_common(m.get(), d->device);
+        tr.mark("init");
         DeviceGuard g(m->device);
         m->n = d->num_states;
         m->n_global = num_global;
@@ -1356,6 +1433,7 @@ static int model_create_impl(const rimdp_model_desc* d, int state_begin, int num
         m->rows.ensure(sizeof(int) * std::max<long long>(1, d->nnz));
         m->lower.ensure(es * std::max<long long>(1, d->nnz));
         m->gap.ensure(es * std::max<long long>(1, d->nnz));
+        tr.mark("alloc");
         CK(cudaMemcpyAsync(m->stateptr.p, d->stateptr, sizeof(int) * (d->num_states + 1), cudaMemcpyHostToDevice,
                            m->stream));
         CK(cudaMemcpyAsync(m->colptr.p, d->colptr, sizeof(long long) * (d->num_cols + 1), cudaMemcpyHostToDevice,
@@ -1365,8 +1443,11 @@ static int model_create_impl(const rimdp_model_desc* d, int state_begin, int num
                         {{m->rows.p, d->rowval, sizeof(int) * (size_t)d->nnz},
                          {m->lower.p, d->lower, es * (size_t)d->nnz},
                          {m->gap.p, d->upper, es * (size_t)d->nnz}});
+        tr.mark("upload");
         DISPATCH(m, prepare, m.get());
+        tr.mark("prepare");
         DISPATCH(m, build_schedule, m.get(), reinterpret_cast<const long long*>(d->colptr));
+        tr.mark("schedule");
         m->device_bytes = (long long)(m->stateptr.bytes + m->colptr.bytes + m->rows.bytes + m->lower.bytes +
                                       m->gap.bytes + m->rem.bytes + m->infeasible.bytes + m->quoted.bytes +
                                       m->maxgap.bytes);
