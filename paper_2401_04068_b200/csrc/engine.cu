@@ -188,6 +188,8 @@ struct rimdp_model {
     DevBuf batch_slots, batch_states, long_states;
     ColumnLists all;                          // every column by class (rimdp_column_values)
     ColumnLists qp;                           // columns of the q-path states (iterations)
+    bool all_is_qp = false;                   // every column is on the q path: `all` is `qp`
+    const ColumnLists& all_lists() const { return all_is_qp ? qp : all; }
     int nbatch = 0, nlong_states = 0;         // fused short-state batches / q-path states
     std::vector<int> h_stateptr;
     std::vector<Infeasible> infeasible_cols;
@@ -560,7 +562,10 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     close_batch();
     tr.mark("classify");
     m->maxlen = maxlen;
-    fill_lists(m, m->all, allc, cls);
+    // every column on the q path (the default: no fused short-state batches): the two sets of lists are the
+    // same, so `all` is not built separately
+    m->all_is_qp = qc.size() == allc.size();
+    if (!m->all_is_qp) fill_lists(m, m->all, allc, cls);
     fill_lists(m, m->qp, qc, cls);
     tr.mark("lists");
     m->nbatch = (int)bstates.size();
@@ -1345,7 +1350,7 @@ int column_values_t(rimdp_model* m, const void* v_in, int pess, void* q_out) {
     CK(cudaMemcpyAsync(s.v[0].p, v_in, sizeof(T) * m->n_global, cudaMemcpyHostToDevice, m->stream));
     s.work.ensure(2 * kWorkKinds * sizeof(unsigned));
     CK(cudaMemsetAsync(s.work.p, 0, 2 * kWorkKinds * sizeof(unsigned), m->stream));
-    launch_columns<T>(m, m->all, s.v[0].as<T>(), s.q.as<T>(), nullptr, pess != 0, s.work.as<unsigned>());
+    launch_columns<T>(m, m->all_lists(), s.v[0].as<T>(), s.q.as<T>(), nullptr, pess != 0, s.work.as<unsigned>());
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(q_out, s.q.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
@@ -1488,9 +1493,10 @@ int rimdp_model_info_get(rimdp_model* m, rimdp_model_info* o) {
     o->max_column_length = m->maxlen;
     o->num_infeasible_columns = (int)m->infeasible_cols.size();
     o->device_bytes = m->device_bytes;
-    o->short_columns = m->all.n_short + m->all.n_tiny[0] + m->all.n_tiny[1] + m->all.n_tiny[2];
-    o->mid_columns = m->all.n_exact + m->all.n_medium[0] + m->all.n_medium[1];
-    o->long_columns = m->all.total_sorted();
+    const ColumnLists& all = m->all_lists();
+    o->short_columns = all.n_short + all.n_tiny[0] + all.n_tiny[1] + all.n_tiny[2];
+    o->mid_columns = all.n_exact + all.n_medium[0] + all.n_medium[1];
+    o->long_columns = all.total_sorted();
     return RIMDP_OK;
 }
 
