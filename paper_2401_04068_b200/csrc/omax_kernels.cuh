@@ -1644,6 +1644,34 @@ omax_select(int nlist, const int* __restrict__ list, const long long* __restrict
 // in tree order: within a few ulps of the reference (1e-12 tests).
 constexpr int kBucketCap = 64;
 
+// Value-bucket histograms: one 64-bit shared atomic per entry, (count << 32) |
+// fixed-point gap mass (the mass of a column is scaled to < 2^31, so it
+// never carries into the count).  RIMDP_HIST64=0: two 32-bit atomics.
+#ifndef RIMDP_HIST64
+#define RIMDP_HIST64 1
+#endif
+__device__ __forceinline__ void hist_add(unsigned* hist, unsigned* hcnt, int bb, unsigned mass) {
+#if RIMDP_HIST64
+    (void)hcnt;
+    atomicAdd(reinterpret_cast<unsigned long long*>(hist) + bb, (1ull << 32) | mass);
+#else
+    atomicAdd(hist + bb, mass);
+    atomicAdd(hcnt + bb, 1u);
+#endif
+}
+__device__ __forceinline__ void hist_get(const unsigned* hist, const unsigned* hcnt, int bb, unsigned& mass,
+                                         unsigned& count) {
+#if RIMDP_HIST64
+    (void)hcnt;
+    const unsigned long long x = reinterpret_cast<const unsigned long long*>(hist)[bb];
+    mass = static_cast<unsigned>(x);
+    count = static_cast<unsigned>(x >> 32);
+#else
+    mass = hist[bb];
+    count = hcnt[bb];
+#endif
+}
+
 template <int LG>
 struct BucketShape {
     static constexpr int Len = 1 << LG;
@@ -1809,8 +1837,7 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             for (int e = 0; e < E; ++e) {
                 if (e * NT + t < L) {
                     const int bb = bucket_of(v[e]);
-                    atomicAdd(hist + bb, static_cast<unsigned>((double)g[e] * sc));
-                    atomicAdd(hcnt + bb, 1u);
+                    hist_add(hist, hcnt, bb, static_cast<unsigned>((double)g[e] * sc));
                 }
             }
         }
@@ -1829,8 +1856,10 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             for (int i = 0; i < PB; ++i) {
                 const int bb = t * PB + i;
                 if (bb < B) {
-                    fm += hist[bb];
-                    fn += hcnt[bb];
+                    unsigned hm, hn;
+                    hist_get(hist, hcnt, bb, hm, hn);
+                    fm += hm;
+                    fn += hn;
                 }
             }
             unsigned long long em = fm, en = fn;
@@ -1860,7 +1889,8 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                 for (int i = 0; i < PB; ++i) {
                     const int bb = t * PB + i;
                     if (bb < B) {
-                        const unsigned hm = hist[bb], hn = hcnt[bb];
+                        unsigned hm, hn;
+                        hist_get(hist, hcnt, bb, hm, hn);
                         if (hn > 0) {
                             if ((double)(em + en) <= R) blo = bb;
                             if ((double)em < R) bhi = bb;
@@ -2059,8 +2089,7 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
             for (int e = 0; e < E; ++e) {
                 if (e * 32 + lane < L) {
                     const int bb = bucket_of(v[e]);
-                    atomicAdd(hist + bb, static_cast<unsigned>((double)g[e] * sc));
-                    atomicAdd(hcnt + bb, 1u);
+                    hist_add(hist, hcnt, bb, static_cast<unsigned>((double)g[e] * sc));
                 }
             }
             __syncwarp();
@@ -2070,8 +2099,10 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
             for (int i = 0; i < PB; ++i) {
                 const int bb = lane * PB + i;
                 if (bb < B) {
-                    fm += hist[bb];
-                    fn += hcnt[bb];
+                    unsigned hm, hn;
+                    hist_get(hist, hcnt, bb, hm, hn);
+                    fm += hm;
+                    fn += hn;
                 }
             }
             unsigned em = fm, en = fn;
@@ -2091,7 +2122,8 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
             for (int i = 0; i < PB; ++i) {
                 const int bb = lane * PB + i;
                 if (bb < B) {
-                    const unsigned hm = hist[bb], hn = hcnt[bb];
+                    unsigned hm, hn;
+                    hist_get(hist, hcnt, bb, hm, hn);
                     if (hn > 0) {
                         if ((double)em + (double)en <= R) blo = bb;
                         if ((double)em < R) bhi = bb;
