@@ -1644,34 +1644,6 @@ omax_select(int nlist, const int* __restrict__ list, const long long* __restrict
 // in tree order: within a few ulps of the reference (1e-12 tests).
 constexpr int kBucketCap = 64;
 
-// Value-bucket histograms: one 64-bit shared atomic per entry, (count << 32) |
-// fixed-point gap mass (the mass of a column is scaled to < 2^31, so it
-// never carries into the count).  RIMDP_HIST64=0: two 32-bit atomics.
-#ifndef RIMDP_HIST64
-#define RIMDP_HIST64 1
-#endif
-__device__ __forceinline__ void hist_add(unsigned* hist, unsigned* hcnt, int bb, unsigned mass) {
-#if RIMDP_HIST64
-    (void)hcnt;
-    atomicAdd(reinterpret_cast<unsigned long long*>(hist) + bb, (1ull << 32) | mass);
-#else
-    atomicAdd(hist + bb, mass);
-    atomicAdd(hcnt + bb, 1u);
-#endif
-}
-__device__ __forceinline__ void hist_get(const unsigned* hist, const unsigned* hcnt, int bb, unsigned& mass,
-                                         unsigned& count) {
-#if RIMDP_HIST64
-    (void)hcnt;
-    const unsigned long long x = reinterpret_cast<const unsigned long long*>(hist)[bb];
-    mass = static_cast<unsigned>(x);
-    count = static_cast<unsigned>(x >> 32);
-#else
-    mass = hist[bb];
-    count = hcnt[bb];
-#endif
-}
-
 template <int LG>
 struct BucketShape {
     static constexpr int Len = 1 << LG;
@@ -1837,7 +1809,8 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             for (int e = 0; e < E; ++e) {
                 if (e * NT + t < L) {
                     const int bb = bucket_of(v[e]);
-                    hist_add(hist, hcnt, bb, static_cast<unsigned>((double)g[e] * sc));
+                    atomicAdd(hist + bb, static_cast<unsigned>((double)g[e] * sc));
+                    atomicAdd(hcnt + bb, 1u);
                 }
             }
         }
@@ -1856,10 +1829,8 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             for (int i = 0; i < PB; ++i) {
                 const int bb = t * PB + i;
                 if (bb < B) {
-                    unsigned hm, hn;
-                    hist_get(hist, hcnt, bb, hm, hn);
-                    fm += hm;
-                    fn += hn;
+                    fm += hist[bb];
+                    fn += hcnt[bb];
                 }
             }
             unsigned long long em = fm, en = fn;
@@ -1889,8 +1860,7 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                 for (int i = 0; i < PB; ++i) {
                     const int bb = t * PB + i;
                     if (bb < B) {
-                        unsigned hm, hn;
-                        hist_get(hist, hcnt, bb, hm, hn);
+                        const unsigned hm = hist[bb], hn = hcnt[bb];
                         if (hn > 0) {
                             if ((double)(em + en) <= R) blo = bb;
                             if ((double)em < R) bhi = bb;
@@ -2089,7 +2059,8 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
             for (int e = 0; e < E; ++e) {
                 if (e * 32 + lane < L) {
                     const int bb = bucket_of(v[e]);
-                    hist_add(hist, hcnt, bb, static_cast<unsigned>((double)g[e] * sc));
+                    atomicAdd(hist + bb, static_cast<unsigned>((double)g[e] * sc));
+                    atomicAdd(hcnt + bb, 1u);
                 }
             }
             __syncwarp();
@@ -2099,10 +2070,8 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
             for (int i = 0; i < PB; ++i) {
                 const int bb = lane * PB + i;
                 if (bb < B) {
-                    unsigned hm, hn;
-                    hist_get(hist, hcnt, bb, hm, hn);
-                    fm += hm;
-                    fn += hn;
+                    fm += hist[bb];
+                    fn += hcnt[bb];
                 }
             }
             unsigned em = fm, en = fn;
@@ -2122,8 +2091,7 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
             for (int i = 0; i < PB; ++i) {
                 const int bb = lane * PB + i;
                 if (bb < B) {
-                    unsigned hm, hn;
-                    hist_get(hist, hcnt, bb, hm, hn);
+                    const unsigned hm = hist[bb], hn = hcnt[bb];
                     if (hn > 0) {
                         if ((double)em + (double)en <= R) blo = bb;
                         if ((double)em < R) bhi = bb;
