@@ -802,7 +802,7 @@ FallbackSlots fallback_slots(rimdp_model* m, int cls, int count) {
 // kernel over the columns it could not bracket tightly (fallback list).
 template <class T, bool P, int LG>
 void launch_bucket_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
-    using Sh = BucketShape<LG>;
+    using Sh = BucketShape<LG, T>;
     auto k = omax_bucket<T, P, LG>;
     const size_t smem = Sh::template smem<T>();
     static bool configured[64] = {};

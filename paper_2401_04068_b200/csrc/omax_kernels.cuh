@@ -1644,10 +1644,16 @@ omax_select(int nlist, const int* __restrict__ list, const long long* __restrict
 // in tree order: within a few ulps of the reference (1e-12 tests).
 constexpr int kBucketCap = 64;
 
-template <int LG>
+// f32 entries take half the registers: 16 entries per thread, half the
+// threads per column, twice the columns in flight per SM (C5 f32 1.98 ->
+// 1.91 ms per iteration).  RIMDP_BUCKET_F32_E16=0: 8 entries as for f64.
+#ifndef RIMDP_BUCKET_F32_E16
+#define RIMDP_BUCKET_F32_E16 1
+#endif
+template <int LG, class TV = double>
 struct BucketShape {
     static constexpr int Len = 1 << LG;
-    static constexpr int E = 8;
+    static constexpr int E = (sizeof(TV) == 4 && RIMDP_BUCKET_F32_E16) ? 16 : 8;
     static constexpr int NT = Len / E;    // 64 .. 1024
     static constexpr int NW = NT / 32;
     static constexpr int B = Len / 4 < 1024 ? Len / 4 : 1024; // ~4 entries per bucket
@@ -1718,7 +1724,7 @@ value_range(int n, const T* __restrict__ V, unsigned long long* __restrict__ slo
 // histogram and the decision words alternate between two buffers so the
 // next column needs no trailing barrier.
 template <class T, bool kPess, int LG>
-__global__ void __launch_bounds__(BucketShape<LG>::NT, BucketShape<LG>::MinBlocks)
+__global__ void __launch_bounds__(BucketShape<LG, T>::NT, BucketShape<LG, T>::MinBlocks)
 omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
             const T* __restrict__ rem, const T* __restrict__ maxgap, const T* __restrict__ V, T* __restrict__ q,
@@ -1726,7 +1732,7 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             int* __restrict__ other_nfallback, const unsigned long long* __restrict__ vrange) {
     using N = Num<T>;
     using Bits = typename N::Bits;
-    using Sh = BucketShape<LG>;
+    using Sh = BucketShape<LG, T>;
     constexpr int E = Sh::E, NT = Sh::NT, NW = Sh::NW, B = Sh::B, CAP = kBucketCap;
     pdl_enter();
     // fallback counters alternate between launches: this launch counts into
