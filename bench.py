@@ -400,17 +400,12 @@ def engine_arm(args, w):
         "scaling": args.scaling_kind,
         "vs_baseline": None,
         "dtype": args.dtype,
-        "data": ("synthetic (reference random_imdp law, seed 1; generated on host, resident in HBM)"
-                 if w["source"] == "reference" else
-                 "synthetic (counter-based generator, seed 1, generated directly in HBM)"),
-        "config": {"workload": w["desc"], "states": n, "columns": n * w["actions"], "transitions": total_nnz,
-                   "parallelism": f"state-sharded x{world} (NCCL all-gather of V)" if world > 1 else "single GPU",
-                   "l2": ("per-iteration inputs (index + bounds, 20 B x transitions) exceed the 126 MB L2; "
-                          "no flush needed" if total_nnz * (4 + 2 * es) > 126e6 else
-                          "inputs fit in L2 (reported as is)"),
-                   "scheduler": {"short_columns": info.short_columns, "exact_long_columns": info.mid_columns,
-                                 "sorted_long_columns": info.long_columns, "max_column_length":
-                                 info.max_column_length}},
+        "data": data_desc(w) + ("; generated on host, resident in HBM" if w["source"] == "reference" else
+                                "; generated directly in HBM"),
+        "config": config_for(w, total_nnz, es, f"state-sharded x{world} (peer exchange of V)" if world > 1
+                             else "single GPU"),
+        "scheduler": {"short_columns": info.short_columns, "exact_long_columns": info.mid_columns,
+                      "sorted_long_columns": info.long_columns, "max_column_length": info.max_column_length},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": kernel_name,
                      "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": kernel_avg,
@@ -430,7 +425,7 @@ def engine_arm(args, w):
         "clocks": clk.summary(),
     }
     if world > 1:
-        out["config"]["shard_nnz_max_over_mean"] = max_nnz / (total_nnz / world)
+        out["shard_nnz_max_over_mean"] = max_nnz / (total_nnz / world)
     if cpu:
         out["cpu_baseline"] = cpu
     if rank == 0:
@@ -445,23 +440,35 @@ def engine_arm(args, w):
 _CPU_MODELS: dict = {}
 
 
-def cpu_sample(w, dtype, budget_s=15.0, which=None):
-    """The reference (oracle/_ref, all host threads; the oracle port on 1 thread
-    if the reference library is absent) on a bounded number of iterations of
-    the workload (configs 4-5: of its law at the `sample` state count)."""
+def cpu_model(w, dtype, states=None):
+    """The workload as a reference model built by the reference itself (oracle/_ref): random_imdp
+    (random_model.hpp:42-101) for configs 2-3, the counter generator's columns through the reference's
+    checked constructors for configs 4-5.  Returns (model, transitions, states)."""
     import oracle
-    which = which or ("ref" if oracle.ref_available() else "port")
-    if which == "port" and not oracle.port_available():
-        oracle.build(ref=False)
-    cores = os.cpu_count() if which == "ref" else 1
-    states = (w.get("sample") or {}).get("states")
-    key = (which, w["desc"], np.dtype(dtype).str)
+    n = states or w["states"]
+    key = (w["desc"], n, np.dtype(dtype).str)
     if key not in _CPU_MODELS:
         t = time.time()
-        arrays = host_arrays(w, dtype, states=states)
-        _CPU_MODELS[key] = (oracle.Model.from_arrays(which, *arrays), int(arrays[1][-1]), len(arrays[0]) - 1)
-        log(f"[bench] cpu model ({which}) built in {time.time() - t:.1f}s")
-    m, nnz, n = _CPU_MODELS[key]
+        if w["source"] == "reference":
+            m = oracle.Model.random(n, w["actions"], w["density"] if n == w["states"] else w["density"] * w["states"] / n,
+                                    w["scale"], w["seed"], dtype=dtype)
+        else:
+            m = oracle.Model.generate(n, w["actions"], law=w["law"], support=w.get("support", 64),
+                                      alpha=w.get("alpha", 1.5), kmax=w.get("kmax", 4096), seed=w["seed"], dtype=dtype)
+        _CPU_MODELS[key] = (m, m.sizes()[2], n)
+        log(f"[bench] reference model ({n} states) built in {time.time() - t:.1f}s")
+    return _CPU_MODELS[key]
+
+
+def cpu_sample(w, dtype, budget_s=15.0):
+    """The reference (oracle/_ref: the unmodified reference headers, value_iteration with workers = 0 = all
+    host threads) on a bounded number of iterations of the workload (configs 4-5: of its law at the
+    `sample` state count)."""
+    import oracle
+    if not oracle.ref_available():
+        oracle.build(port=False)
+    states = (w.get("sample") or {}).get("states")
+    m, nnz, n = cpu_model(w, dtype, states)
     kw = plan_kw(w, n, dtype)
 
     def run(k):
@@ -479,41 +486,61 @@ def cpu_sample(w, dtype, budget_s=15.0, which=None):
     k = max(1, min(200, int(budget_s / max(one, 1e-6))))
     secs = run(k)
     scope = "the same workload" if not states else f"the same law at {n} states ({nnz} transitions)"
-    return {"value": nnz * k / secs, "unit": "transitions/s", "cores": cores,
-            "kind": "reference" if which == "ref" else "port",
+    return {"value": nnz * k / secs, "unit": "transitions/s", "cores": os.cpu_count(), "kind": "reference",
             "sample": f"{k} Bellman iterations of {scope} (finite-horizon {k}, same goal/reward and modes), "
-                      f"value_iteration with workers=0, {secs:.2f}s"}
+                      f"reference value_iteration with workers=0 on {os.cpu_count()} host threads, {secs:.2f}s"}
 
 
 def reference_arm(args, w):
+    """The reference's own CPU implementation (oracle/_ref) on this arm's config; rank 0 only at N > 1.
+    Imports nothing from the engine package."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     dtype = np.float64 if args.dtype == "f64" else np.float32
+    es = np.dtype(dtype).itemsize
     target = min(3.0, 120.0 / max(1, args.steps))
     cpu = None
-    for _ in range(1 if args.warmup else 0):
+    for _ in range(args.warmup and 1):
         cpu = cpu_sample(w, dtype, budget_s=target)
     vals = []
     for _ in range(args.steps):
         cpu = cpu_sample(w, dtype, budget_s=target)
         vals.append(cpu["value"])
     v = statistics.median(vals)
-    nnz_full = None
-    if w["source"] == "reference":
-        from paper_2401_04068_b200 import engine
-        nnz_full = int(engine.random_imdp(w["states"], w["actions"], w["density"], w["scale"], w["seed"])[1][-1])
+    nnz_full = cpu_model(w, dtype)[1] if w["source"] == "reference" else full_transitions(w)
     cpu["value"] = v
     out = {"impl": "reference", "metric": "transitions/sec per Bellman iteration", "value": v,
-           "unit": "transitions/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": (nnz_full / v * 1e3) if nnz_full else None,
+           "unit": "transitions/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": nnz_full / v * 1e3,
            "higher_is_better": True, "scaling": args.scaling_kind, "vs_baseline": None, "dtype": args.dtype,
-           "data": "synthetic (same generator and seed as the engine arm)",
-           "config": {"workload": w["desc"], "states": w["states"], "transitions": nnz_full,
-                      "parallelism": f"host threads ({os.cpu_count()})"},
+           "data": data_desc(w),
+           "config": config_for(w, nnz_full, es, f"reference CPU, {os.cpu_count()} host threads"),
            "cpu_baseline": cpu,
            "e2e": {"value": v, "unit": "transitions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def full_transitions(w):
+    """Transitions of a counter-generated workload at full size (configs 4-5): the generator's column
+    lengths, summed on the host without building the columns."""
+    import oracle
+    return oracle.generate_nnz(w["states"], w["actions"], law=w["law"], support=w.get("support", 64),
+                               alpha=w.get("alpha", 1.5), kmax=w.get("kmax", 4096), seed=w["seed"])
+
+
+def data_desc(w):
+    return ("synthetic (reference random_imdp law, seed 1)" if w["source"] == "reference" else
+            "synthetic (counter-based generator, seed 1)")
+
+
+def config_for(w, transitions, es, parallelism):
+    """The `config` object of both arms (identical keys; only `parallelism` differs)."""
+    return {"workload": w["desc"], "states": w["states"], "columns": w["states"] * w["actions"],
+            "transitions": transitions, "parallelism": parallelism,
+            "l2": ("per-iteration inputs (index + bounds, 20 B x transitions) exceed the 126 MB L2; no flush needed"
+                   if transitions and transitions * (4 + 2 * es) > 126e6 else "inputs fit in L2 (reported as is)")}
 
 
 def main():
@@ -530,6 +557,16 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak (C2 law, N x the states) or strong (fixed model)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver's own launch sets WORLD_SIZE)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        log("[bench] spawning", args.gpus, "ranks:", " ".join(cmd))
+        sys.exit(subprocess.call(cmd))
     if args.warmup < 3:
         args.warmup = 3
     w, args.scaling_kind = scaled_workload(WORKLOADS[args.config], int(os.environ.get("WORLD_SIZE", "1")),

@@ -176,6 +176,28 @@ class Model:
         return cls("ref", h, dtype)
 
     @classmethod
+    def generate(cls, states, actions, *, law=0, support=64, alpha=1.5, kmax=4096, lower_scale=None,
+                 upper_scale=None, seed=1, dtype=np.float64):
+        """A counter-generator workload (configs 4-5, csrc/generator.cuh host build) built through the
+        reference's checked constructors; ref only.  Scales default as engine.gen_config."""
+        if law == 0:
+            k = min(support, states)
+            lower_scale = 1.0 / k if lower_scale is None else lower_scale
+            upper_scale = 1.0 - 1.0 / k if upper_scale is None else upper_scale
+        else:
+            lower_scale = 0.5 if lower_scale is None else lower_scale
+            upper_scale = 3.0 if upper_scale is None else upper_scale
+        L = _lib("ref")
+        h = C.c_void_p()
+        err = Err()
+        st = L.fn("model_generate", dtype)(int(states), int(actions), int(law), int(support), C.c_double(alpha),
+                                           int(kmax), C.c_double(lower_scale), C.c_double(upper_scale),
+                                           C.c_ulonglong(seed), C.byref(h), C.byref(err))
+        if st:
+            raise OracleError(st, err)
+        return cls("ref", h, dtype)
+
+    @classmethod
     def read_native(cls, path, dtype=np.float64):
         """io::read_native_model (io/native.hpp:457-561) of the reference; ref only."""
         L = _lib("ref")
@@ -278,6 +300,14 @@ class Model:
         if st:
             raise OracleError(st, err)
         return ov, oc
+
+
+def generate_nnz(states, actions, *, law=0, support=64, alpha=1.5, kmax=4096, seed=1) -> int:
+    """Transitions of a counter-generator workload (column lengths only, any size)."""
+    f = _lib("ref").lib.ref_generate_nnz
+    f.restype = C.c_longlong
+    return int(f(int(states), int(actions), int(law), int(support), C.c_double(alpha), int(kmax),
+                 C.c_ulonglong(seed)))
 
 
 def robust_expectation(which, rows, lower, upper, values, pessimistic, with_p=False):

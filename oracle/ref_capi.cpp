@@ -17,11 +17,17 @@
 //   oracle::robust_expectation (LP)      tests/oracle.hpp:28-80
 //   oracle::random_feasible_column       tests/oracle.hpp:193-217
 //   io::write_native_model / read_native_model  io/native.hpp:424-561
+// The one non-reference input is the counter-based workload generator of
+// BASELINE configs 4-5 (paper_2401_04068_b200/csrc/generator.cuh, host-side
+// and header-only: a workload, not the algorithm), so bench.py's reference
+// arm can build those models without loading the engine library.
 
 #include "rimdp/io/native.hpp"
 #include "rimdp/random_model.hpp"
 #include "rimdp/solver.hpp"
 #include "oracle.hpp" // proj/tests/oracle.hpp
+
+#include "generator.cuh" // workload generator of configs 4-5 (host build)
 
 #include <cstdint>
 #include <cstring>
@@ -186,6 +192,37 @@ int from_arrays(int n, int ncols, const int* stateptr, const int* colptr, const 
             auto t = rimdp::IntervalProbabilities<V>::from_aligned_unchecked(n, ncols, cp, rv, lo, up);
             m->mdp = rimdp::IntervalMDP<V>::from_parts_unchecked(std::move(t), sp, labels);
         }
+        *out = static_cast<ModelBase*>(m);
+    });
+}
+
+// A counter-generator workload (configs 4-5 law, rimdp_gen::write_column)
+// built through the reference's own checked constructors.
+template <class V>
+int generate_model(int states, int actions, int law, int support, double alpha, int kmax, double lower_scale,
+                   double upper_scale, unsigned long long seed, void** out, ref_err* err) {
+    ErrOut e{err ? err->msg : nullptr, err ? 512 : 0, nullptr, nullptr, nullptr, nullptr};
+    return guarded(e, [&] {
+        rimdp_gen::Params p{states, actions, law, support, kmax, lower_scale, upper_scale, seed};
+        std::vector<uint64_t> cdf;
+        if (law == 1) cdf = rimdp_gen::power_law_cdf(kmax, alpha);
+        const index_t ncols = static_cast<index_t>(states) * actions;
+        std::vector<index_t> cp(ncols + 1, 0), sp(states + 1);
+        for (index_t c = 0; c < ncols; ++c) cp[c + 1] = cp[c] + rimdp_gen::column_length(p, cdf.data(), c);
+        for (int s = 0; s <= states; ++s) sp[s] = s * actions;
+        std::vector<index_t> rv(cp[ncols]);
+        std::vector<V> lo(cp[ncols]), up(cp[ncols]);
+        std::vector<std::int32_t> r32(4096 * 2);
+        for (index_t c = 0; c < ncols; ++c) {
+            const int k = cp[c + 1] - cp[c];
+            if ((int)r32.size() < k) r32.resize(k);
+            rimdp_gen::write_column<V>(p, c, k, r32.data(), lo.data() + cp[c], up.data() + cp[c]);
+            for (int i = 0; i < k; ++i) rv[cp[c] + i] = r32[i];
+        }
+        auto labels = positional_labels(sp);
+        auto m = new Model<V>;
+        auto t = rimdp::IntervalProbabilities<V>::from_aligned(states, ncols, cp, rv, lo, up);
+        m->mdp = rimdp::IntervalMDP<V>::from_parts(std::move(t), sp, labels);
         *out = static_cast<ModelBase*>(m);
     });
 }
@@ -389,6 +426,25 @@ int ref_model_random_f64(int states, int actions, double density, double scale,
 int ref_model_random_f32(int states, int actions, double density, double scale,
                          unsigned long long seed, int point, void** out, ref_err* err) {
     return random_model<float>(states, actions, density, scale, seed, point, out, err);
+}
+int ref_model_generate_f64(int states, int actions, int law, int support, double alpha, int kmax, double lscale,
+                           double uscale, unsigned long long seed, void** out, ref_err* err) {
+    return generate_model<double>(states, actions, law, support, alpha, kmax, lscale, uscale, seed, out, err);
+}
+int ref_model_generate_f32(int states, int actions, int law, int support, double alpha, int kmax, double lscale,
+                           double uscale, unsigned long long seed, void** out, ref_err* err) {
+    return generate_model<float>(states, actions, law, support, alpha, kmax, lscale, uscale, seed, out, err);
+}
+// Transitions of a generator workload at any size (column lengths only).
+long long ref_generate_nnz(int states, int actions, int law, int support, double alpha, int kmax,
+                           unsigned long long seed) {
+    rimdp_gen::Params p{states, actions, law, support, kmax, 0.0, 0.0, seed};
+    std::vector<uint64_t> cdf;
+    if (law == 1) cdf = rimdp_gen::power_law_cdf(kmax, alpha);
+    long long z = 0;
+    const long long ncols = static_cast<long long>(states) * actions;
+    for (long long c = 0; c < ncols; ++c) z += rimdp_gen::column_length(p, cdf.data(), c);
+    return z;
 }
 void ref_model_free(void* h) { delete static_cast<ModelBase*>(h); }
 

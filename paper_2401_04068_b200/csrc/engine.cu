@@ -1130,7 +1130,9 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     if (m->l2_persist) set_value_window(m, vin, sizeof(T) * (size_t)m->n_global);
     launch_columns<T>(m, m->qp, vin, s.q.as<T>(), ctl, s.pess, work);
     if (ev) CK(cudaEventRecord(ev[2], m->stream));
-    if (m->nlong_states > 0) {
+    if (m->nlong_states > 0 || m->nbatch == 0) {
+        // a shard that owns no states still runs one block: its epilogue advances ctl->k and the residual
+        // slots, so the sharded stop test and the solve outputs see iteration k
         a.finalize = 1;
         launch_pdl(m->pdl_now, action_reduce<T>, grid_for(m->nlong_states, 256, m->sm_count, 8), 256, 0, m->stream,
             a, m->nlong_states, m->long_states.as<int>(), s.q.as<T>(), vin, vout, rw, (T)s.discount, (T)s.eps, ctl);
@@ -1216,7 +1218,7 @@ void advance_t(rimdp_model* m, long long iters) {
     for (long long i = 0; i < iters; ++i) {
         const long long k = s.launched + 1;
         if (s.finite && k > s.horizon) break;
-        if (!s.finite && k > s.max_iterations) break;
+        if (!s.finite && k > std::max(1LL, s.max_iterations)) break; // iterate() always runs step 1
         launch_iteration<T>(m, k, chosen, chosen_td);
         s.launched = k;
     }
@@ -1270,6 +1272,34 @@ void prepare_chosen(rimdp_model* m, const rimdp_outputs* o, const rimdp_plan* p)
     }
 }
 
+// How many iterations to enqueue before the next poll.  Finite horizons are
+// capped exactly by advance_t.  For infinite horizons the residual decays
+// geometrically near convergence (contraction), so the rate measured between
+// two polls predicts the iteration at which max residual <= eps; enqueueing
+// up to that prediction (+1) keeps the no-op launches after the device stop
+// test (kernels return at their first instruction once `done` is set) to a
+// handful instead of a whole doubling chunk.
+struct ChunkPlanner {
+    bool finite;
+    double eps;
+    long long chunk = 8, last_k = 0;
+    double last_res = -1.0;
+    explicit ChunkPlanner(const rimdp_plan* p) : finite(p->finite != 0), eps(p->eps) {}
+    long long next() const { return chunk; }
+    void observe(long long k, double res) {
+        long long want = std::min<long long>(chunk * 2, kMaxChunk);
+        if (!finite && last_res > 0.0 && res > 0.0 && res < last_res && k > last_k && eps > 0.0) {
+            const double rate = std::log(res / last_res) / (double)(k - last_k); // log rho < 0
+            const double need = std::log(eps / res) / rate;                        // iterations to eps
+            if (std::isfinite(need)) want = std::max<long long>(1, std::min<long long>((long long)need + 1, want));
+        }
+        chunk = want;
+        last_k = k;
+        last_res = res;
+    }
+    static constexpr long long kMaxChunk = 64;
+};
+
 template <class T>
 int solve_t(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
     const bool will_step = p->finite ? p->horizon > 0 : true;
@@ -1281,7 +1311,7 @@ int solve_t(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
     upload_plan<T>(m, p);
     prepare_chosen(m, o, p);
     tr.mark("plan");
-    const long long total = p->finite ? p->horizon : p->max_iterations;
+    const long long total = p->finite ? p->horizon : std::max<long long>(1, p->max_iterations);
     long long k = 0;
     Ctl c{};
     if (o && o->on_iteration) {
@@ -1295,15 +1325,18 @@ int solve_t(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
             if (c.done) break;
         }
     } else {
-        long long chunk = 8;
+        ChunkPlanner cp(p);
         while (!c.done && m->s.launched < total) {
-            advance_t<T>(m, chunk);
+            advance_t<T>(m, cp.next());
             c = read_ctl(m);
-            chunk = std::min<long long>(chunk * 2, 64);
+            cp.observe(c.k, c.res_last);
         }
         k = c.k;
     }
     tr.mark("iterations");
+    // omax_long (RIMDP_LONG=exact) tracks at most kMaxPartial positions that received a partial share;
+    // more than one needs avail > 0 to survive a consumed += gap >= avail step through rounding, so the
+    // overflow is only reachable by adversarial bounds, and it is reported instead of summed wrongly
     if (c.status == 2) return fail(RIMDP_ERR_INTERNAL, "partial-assignment overflow in a long column");
     finish_t<T>(m, o, k);
     tr.mark("finish");
@@ -1536,6 +1569,9 @@ int rimdp_solve_begin(rimdp_model* m, const rimdp_plan* p) {
     if (int st = check_plan(m, p)) return st;
     return guarded([&]() -> int {
         DeviceGuard g(m->device);
+        // the same InfeasibleColumn report as rimdp_solve (omax.hpp:72-80): the first column a step evaluates
+        if (!p->finite || p->horizon > 0)
+            if (const Infeasible* f = first_evaluated_infeasible(m, p)) return report_infeasible(f, m->dtype);
         m->s.record_only = false;
         rimdp_outputs none{};
         prepare_chosen(m, &none, p);
@@ -1733,17 +1769,8 @@ int gen_setup(const rimdp_gen_config* cfg, GenSetup& g) {
     } else if (cfg->law == 1) {
         if (cfg->kmax <= 0 || cfg->kmax > rimdp_gen::kMaxK)
             return fail(RIMDP_ERR_INVALID_ARGUMENT, "kmax must be in [1, %d]", rimdp_gen::kMaxK);
-        // cdf[k-1] = floor(2^64 P(K <= k)), P(K = k) ~ k^-alpha
-        std::vector<long double> w(cfg->kmax);
-        long double z = 0;
-        for (int k = 1; k <= cfg->kmax; ++k) z += (w[k - 1] = powl((long double)k, -(long double)cfg->alpha));
-        g.cdf.resize(cfg->kmax);
-        long double acc = 0;
-        for (int k = 1; k <= cfg->kmax; ++k) {
-            acc += w[k - 1];
-            const long double f = acc / z * 18446744073709551616.0L;
-            g.cdf[k - 1] = (k == cfg->kmax || f >= 18446744073709551615.0L) ? ~0ull : (unsigned long long)f;
-        }
+        const std::vector<uint64_t> cdf = rimdp_gen::power_law_cdf(cfg->kmax, cfg->alpha);
+        g.cdf.assign(cdf.begin(), cdf.end());
     } else {
         return fail(RIMDP_ERR_INVALID_ARGUMENT, "unknown law %d", cfg->law);
     }

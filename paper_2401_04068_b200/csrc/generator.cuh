@@ -24,7 +24,9 @@
 //     attempt counter (the reference generator's rejection, random_model.hpp:62-86).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
+#include <vector>
 
 #ifdef __CUDACC__
 #define RIMDP_HD __host__ __device__ __forceinline__
@@ -151,6 +153,25 @@ RIMDP_HD uint32_t write_column(const Params& p, int64_t c, int k, int32_t* rows,
             return attempt;
         }
     }
+}
+
+// Host only: the law-1 threshold table, cdf[k-1] = floor(2^64 P(K <= k)) with
+// P(K = k) ~ k^-alpha on [1, kmax] (long double accumulation; the last
+// threshold saturates so every draw lands in [1, kmax]).  Shared by the
+// engine (csrc/engine.cu) and the CPU checker's workload builder
+// (oracle/ref_capi.cpp), so both produce the same columns.
+inline std::vector<uint64_t> power_law_cdf(int kmax, double alpha) {
+    std::vector<long double> w(kmax);
+    long double z = 0;
+    for (int k = 1; k <= kmax; ++k) z += (w[k - 1] = powl((long double)k, -(long double)alpha));
+    std::vector<uint64_t> cdf(kmax);
+    long double acc = 0;
+    for (int k = 1; k <= kmax; ++k) {
+        acc += w[k - 1];
+        const long double f = acc / z * 18446744073709551616.0L;
+        cdf[k - 1] = (k == kmax || f >= 18446744073709551615.0L) ? ~0ull : (uint64_t)f;
+    }
+    return cdf;
 }
 
 } // namespace rimdp_gen

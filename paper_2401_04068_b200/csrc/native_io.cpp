@@ -233,6 +233,13 @@ std::unique_ptr<Model<V>> read_model(const std::string& path) {
             in.model_error(SE, "value arrays do not match colptr");
         for (int64_t j = 0; j < ncols; ++j) {
             if (cp[j] > cp[j + 1]) in.model_error(SE, "colptr not monotone", -1, j);
+            if (cp[j + 1] > static_cast<int64_t>(rv.size())) {
+                // a later pointer decreases (front/back are checked): report that column instead of
+                // reading past the row array (the reference's loop would read out of bounds here)
+                int64_t d = j + 1;
+                while (d < ncols && cp[d] <= cp[d + 1]) ++d;
+                in.model_error(SE, "colptr not monotone", -1, d);
+            }
             for (int64_t k = cp[j]; k < cp[j + 1]; ++k)
                 if (k > cp[j] && rv[k] <= rv[k - 1])
                     in.model_error(SE, "row indices not strictly increasing within column", -1, j, rv[k]);

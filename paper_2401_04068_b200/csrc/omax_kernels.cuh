@@ -8,14 +8,23 @@
 //   per state    bellman_step_impl (bellman.hpp:75-118)
 //   per iterate  reward update, residual, stop test (solver.hpp:107-134)
 //
-// Every floating-point operation the reference performs is performed here
-// in the same order with the same rounding, so results are bit-identical:
-//   * the adversary ordering is found by exact integer argmin over
+// Arithmetic order:
+//   * every kernel makes the reference's greedy decisions exactly: the
+//     adversary ordering is found by exact integer argmin over
 //     (order-preserving key of V[row], position) — position order is row
-//     order because rows are strictly increasing (csc.hpp:98-101);
-//   * `consumed` is accumulated sequentially along that ordering;
-//   * the expectation is summed sequentially in row order by one lane per
-//     column, from products staged in shared memory.
+//     order because rows are strictly increasing (csc.hpp:98-101) — and
+//     `consumed` is accumulated sequentially along that ordering up to the
+//     cut;
+//   * the row-order kernels (omax_tiny, omax_short, omax_medium, omax_long,
+//     action_reduce, bellman_short) also sum the expectation sequentially in
+//     row order with separate round-to-nearest mul/add, so their results
+//     are bit-identical to the reference;
+//   * the single-pass / selection kernels (omax_long_tree, omax_wbucket,
+//     omax_bucket, omax_select, omax_sorted) sum the expectation — and the
+//     last four the gaps below the cut — in tree order (the paper's parallel
+//     form): within a few ulps (north_star: 1e-12 per iteration).  The
+//     scheduler routes float32 models to the row-order kernels only (see
+//     engine.cu column_class), where a few ulps exceed the stop tolerance.
 #pragma once
 
 #include "numeric.cuh"

@@ -4,6 +4,7 @@ Run in the dev container (needs /root/reference and oracle/_ref):
 
     python tests/golden/make_golden.py            # small fixtures
     python tests/golden/make_golden.py --c2 --c3  # config-2/3 convergence digests (minutes)
+    python tests/golden/make_golden.py --c5s      # config-5 law at 30000 states, f64 + f32 (a minute)
 
 Every number comes from the unmodified reference headers compiled by
 oracle/Makefile (oracle/_ref/librimdp_ref.so): random_imdp / random_point_imdp
@@ -216,6 +217,7 @@ def big(which: str):
         modes = [(0, 1), (1, 1)]
     rm = Model.random(**cfg)
     res = {"config": cfg, "goal": [goal[0], goal[-1] + 1], "runs": {}}
+    full = {}
     for mx, pe in modes:
         pr = Problem(oracle.INFINITE_REACH, reach=goal, eps=1e-6, pessimistic=pe, maximize=mx)
         t = time.time()
@@ -231,14 +233,51 @@ def big(which: str):
             "sample_hex": [float(v[i]).hex() for i in range(0, cfg["states"], cfg["states"] // 16)],
         }
         print(which, mx, pe, res["runs"][f"m{mx}p{pe}"]["iterations"], f"{dt:.1f}s", flush=True)
+        if which == "c3":  # 2000 states: the whole vectors are small enough to keep
+            full[f"m{mx}p{pe}/values"] = v
+            full[f"m{mx}p{pe}/residual"] = out["residual"]
+            full[f"m{mx}p{pe}/policy"] = out["policy"].astype(np.int32)
     with open(os.path.join(OUT, f"{which}.json"), "w") as f:
         json.dump(res, f, indent=1)
+    if full:
+        np.savez_compressed(os.path.join(OUT, f"{which}_full.npz"), **full)
+
+
+def c5_scaled(states=30000):
+    """BASELINE config 5's law (power-law successor counts k^-1.5 on [1, 4096], 4 actions, discounted reward
+    gamma = 0.95, eps = 1e-6, Pessimistic + Maximize synthesis) at `states` states, float64 and float32:
+    the counter generator's columns (oracle.Model.generate == engine.generate_host) solved by the reference's
+    control_synthesis.  Whole vectors and policies are stored (c5s.npz)."""
+    import time
+    res = {"config": dict(states=states, actions=4, law=1, alpha=1.5, kmax=4096, seed=1, discount=0.95,
+                          eps=1e-6, rewards="np.random.default_rng(1).random(states).astype(dtype)"),
+           "runs": {}}
+    full = {}
+    for dt in (np.float64, np.float32):
+        name = "f64" if dt == np.float64 else "f32"
+        rm = Model.generate(states, 4, law=1, alpha=1.5, kmax=4096, seed=1, dtype=dt)
+        r = np.random.default_rng(1).random(states).astype(dt)
+        pr = Problem(oracle.INFINITE_REWARD, rewards=r, discount=0.95, eps=1e-6, pessimistic=True, maximize=True)
+        t = time.time()
+        out = rm.solve(pr, synthesize=True)
+        res["runs"][name] = {"iterations": int(out["iterations"]), "seconds": time.time() - t,
+                             "threads": os.cpu_count(), "nnz": int(rm.sizes()[2]),
+                             "values_sha256": digest(out["values"]), "residual_sha256": digest(out["residual"]),
+                             "policy_sha256": digest(out["policy"].astype(np.int32))}
+        full[f"{name}/values"] = out["values"]
+        full[f"{name}/residual"] = out["residual"]
+        full[f"{name}/policy"] = out["policy"].astype(np.int32)
+        print("c5s", name, out["iterations"], flush=True)
+    with open(os.path.join(OUT, "c5s.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    np.savez_compressed(os.path.join(OUT, "c5s.npz"), **full)
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true")
     ap.add_argument("--c3", action="store_true")
+    ap.add_argument("--c5s", action="store_true")
     ap.add_argument("--no-small", action="store_true")
     a = ap.parse_args()
     oracle.build()
@@ -248,3 +287,5 @@ if __name__ == "__main__":
         big("c2")
     if a.c3:
         big("c3")
+    if a.c5s:
+        c5_scaled()

@@ -1,11 +1,14 @@
 """Full-size parity of BASELINE configs 2 and 3 against the reference's own
-solves (tests/golden/c2.json, c3.json: iteration counts, SHA-256 of the value
-and residual vectors, sampled values as hex; make_golden.py).
+solves (tests/golden/c2.json, c3.json + c3_full.npz, made by make_golden.py
+from oracle/_ref): iteration counts, SHA-256 of the value / residual vectors
+and of the synthesized strategy (column per state), and C3's whole value
+vectors and strategies.
 
-C2 runs on the bit-exact short-column kernels: identical hashes.  C3's
-few-pick 2000-entry columns run on the single-pass tree-order kernel by
-default (north_star bar: identical iterations, 1e-9 at convergence) and on
-the row-order kernel with RIMDP_LONG=exact (identical hashes)."""
+C2 runs on the bit-exact short-column kernels: identical hashes, including
+the strategy.  C3's few-pick 2000-entry columns run on the single-pass
+tree-order kernel by default (north_star bar: identical iterations, 1e-9 at
+convergence, strategies equal wherever the action gap exceeds the tolerance)
+and on the row-order kernel with RIMDP_LONG=exact (identical hashes)."""
 import hashlib
 import json
 import os
@@ -17,28 +20,31 @@ from paper_2401_04068_b200 import engine, problems as P
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CONV_TOL = 1e-9      # north_star: values at convergence
+GAP_TOL = 1e-12      # strategies must agree where the best two actions differ by more than this (per step)
 
 
-def solve(cfg, run_key, env=None):
+def model(cfg, env=None):
     states, actions, density, scale = cfg
     arrays = engine.random_imdp(states, actions, density, scale, seed=1)
     old = {k: os.environ.get(k) for k in (env or {})}
     os.environ.update(env or {})
     try:
-        m = engine.DeviceModel.from_csc(*arrays)
+        return engine.DeviceModel.from_csc(*arrays), arrays
     finally:
         for k, v in old.items():
             if v is None:
                 os.environ.pop(k)
             else:
                 os.environ[k] = v
+
+
+def synthesize(m, arrays, states, run_key):
     goal = list(range(states - states // 100, states))
     maxi, pess = int(run_key[1]), int(run_key[3])
     spec = P.Specification(P.InfiniteTimeReachability(goal, 1e-6), P.PESSIMISTIC if pess else P.OPTIMISTIC,
                            P.MAXIMIZE if maxi else P.MINIMIZE)
-    vf = P.value_iteration(m, spec)
-    m.close()
-    return vf
+    return P.control_synthesis(m, spec, arrays[0])
 
 
 def golden(name):
@@ -50,21 +56,48 @@ def sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
+def decisive_states(m, arrays, values, pess, maxi):
+    """States whose best and second-best actions differ by more than GAP_TOL at `values`, the iterate the
+    last step chose from (single-action states are decisive trivially: their column is fixed)."""
+    q = m.column_values(values, pess)
+    sp = arrays[0]
+    n = len(sp) - 1
+    ok = np.ones(n, bool)
+    for s in range(n):
+        qs = np.sort(q[sp[s]:sp[s + 1]])
+        if len(qs) > 1:
+            a, b = (qs[-1], qs[-2]) if maxi else (qs[0], qs[1])
+            ok[s] = abs(a - b) > GAP_TOL
+    return ok
+
+
 def test_c2_full_size_bit_exact():
+    m, arrays = model((100000, 4, 32.0 / 100000, 1.0 / 32))
     for key, run in golden("c2").items():
-        vf = solve((100000, 4, 32.0 / 100000, 1.0 / 32), key)
+        policy, vf = synthesize(m, arrays, 100000, key)
         assert vf.iterations == run["iterations"], key
         assert sha(vf.values) == run["values_sha256"] and sha(vf.residual) == run["residual_sha256"], key
+        assert sha(policy.columns.astype(np.int32)) == run["policy_sha256"], key
+    m.close()
 
 
 @pytest.mark.parametrize("mode", ["default", "exact"])
 def test_c3_full_size(mode):
+    full = np.load(os.path.join(GOLDEN, "c3_full.npz"))
+    m, arrays = model((2000, 10, 1.0, 1.0 / 2000), {"RIMDP_LONG": "exact"} if mode == "exact" else None)
     for key, run in golden("c3").items():
-        vf = solve((2000, 10, 1.0, 1.0 / 2000), key, {"RIMDP_LONG": "exact"} if mode == "exact" else None)
+        policy, vf = synthesize(m, arrays, 2000, key)
+        ref_v, ref_pol = full[f"{key}/values"], full[f"{key}/policy"]
         assert vf.iterations == run["iterations"], key
-        idx = np.array(run["sample_idx"])
-        ref = np.array([float.fromhex(h) for h in run["sample_hex"]])
-        assert np.abs(vf.values[idx] - ref).max() <= 1e-9, key
-        assert abs(vf.values.min() - run["vmin"]) <= 1e-9 and abs(vf.values.max() - run["vmax"]) <= 1e-9
+        assert np.abs(vf.values - ref_v).max() <= CONV_TOL, key       # all 2000 values
+        assert sha(ref_v) == run["values_sha256"]                       # the fixture is the digested run
         if mode == "exact":
             assert sha(vf.values) == run["values_sha256"] and sha(vf.residual) == run["residual_sha256"], key
+            assert np.array_equal(policy.columns, ref_pol), key
+        else:
+            # reachability from the goal indicator is monotone, so V_{K-1} = V_K - residual exactly (Sterbenz)
+            prev = vf.values - vf.residual
+            sure = decisive_states(m, arrays, prev, int(key[3]), int(key[1]))
+            assert sure.sum() > 0.5 * len(sure)
+            assert np.array_equal(policy.columns[sure], ref_pol[sure]), key
+    m.close()
