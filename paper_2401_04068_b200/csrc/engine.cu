@@ -198,6 +198,7 @@ struct rimdp_model {
     int short_blocks_per_sm = 4;
     bool bitonic = false;                     // many-pick long columns: bitonic sort instead of selection
     bool long_exact = false;                  // few-pick long columns: row-order omax_long (RIMDP_LONG=exact)
+    bool exact_sorted = false;                // many-pick long columns: sorted + sequential sums (float32 default)
     bool bucket = true;                       // columns > 256 entries: value buckets first (RIMDP_BUCKET=0: off)
     DevBuf fallback[kSortedClasses];          // per size class: [count A, count B, columns...] omax_bucket -> omax_select
     int fallback_parity[kSortedClasses] = {}; // which count the next omax_bucket launch of the class uses
@@ -421,6 +422,11 @@ void upload_list(rimdp_model* m, DevBuf& buf, const std::vector<U>& v) {
 // Routing mode for long columns (tests): RIMDP_LONG=exact (every long column
 // on the exact warp kernel), sorted (every one on the bitonic CTA kernel),
 // select (every one on the selection kernels, no value buckets).
+bool env_flag(const char* name) {
+    const char* e = getenv(name);
+    return e && atoi(e) != 0;
+}
+
 int long_mode() {
     const char* e = getenv("RIMDP_LONG");
     if (!e) return 0;
@@ -508,6 +514,13 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     const int mode = long_mode();
     m->bitonic = mode == 2;
     m->long_exact = mode == 1;
+    // float32: one ulp of the values is of the order of the stop tolerance, so a tree-order sum can move
+    // the iteration at which max residual <= eps; every float32 column therefore takes a row-order kernel
+    // (bit-identical to the reference) unless RIMDP_F32_FAST=1 (tree-order, within a few ulps)
+    if (std::is_same<T, float>::value && !env_flag("RIMDP_F32_FAST")) {
+        m->long_exact = m->long_exact || mode == 0;
+        m->exact_sorted = mode == 0 || mode == 1;
+    }
     {
         // RIMDP_LONG=select (tests) keeps every many-pick column on the selection kernels
         const char* eb = getenv("RIMDP_BUCKET");
@@ -736,10 +749,10 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     s.record_only = p->external_stop != 0;
 }
 
-template <class T, bool P, int LG>
+template <class T, bool P, int LG, bool X = false>
 void launch_sorted_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
     using Sh = SortedShape<LG>;
-    auto k = omax_sorted<T, P, LG>;
+    auto k = omax_sorted<T, P, LG, X>;
     const size_t smem = Sh::template smem<T>();
     static bool configured[64] = {};
     static int per_sm[64] = {};
@@ -849,7 +862,9 @@ void launch_sorted(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* 
     if constexpr (LG <= kSortedMaxLog) {
         const int i = LG - kSortedMinLog;
         if (L.n_sorted[i] > 0) {
-            if (m->bitonic)
+            if (m->exact_sorted)
+                launch_sorted_class<T, P, LG, true>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+            else if (m->bitonic)
                 launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else if (LG >= 9 && m->bucket)
                 launch_bucket_class<T, P, (LG >= 9 ? LG : 9)>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
@@ -1004,7 +1019,9 @@ void launch_sorted_fanout(rimdp_model* m, const ColumnLists& L, const T* V, T* q
         const int i = LG - kSortedMinLog;
         if (L.n_sorted[i] > 0) {
             f.pick();
-            if (m->bitonic)
+            if (m->exact_sorted)
+                launch_sorted_class<T, P, LG, true>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+            else if (m->bitonic)
                 launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else if (LG >= 9 && m->bucket)
                 launch_bucket_class<T, P, (LG >= 9 ? LG : 9)>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
@@ -1025,7 +1042,7 @@ void launch_value_range(rimdp_model* m, const ColumnLists& L, const T* V) {
     bool need = false;
     for (int i = 0; i < kSortedClasses; ++i) need = need || L.n_sorted[i] > 0;
     m->vrange_cur = nullptr;
-    if (!need || m->bitonic || !m->bucket) return;
+    if (!need || m->bitonic || m->exact_sorted || !m->bucket) return;
     if (!m->vrange.p) {
         m->vrange.ensure(4 * sizeof(unsigned long long));
         const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};

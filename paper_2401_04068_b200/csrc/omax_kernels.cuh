@@ -1129,7 +1129,13 @@ struct SortedShape {
     static constexpr size_t smem() { return N * (8 + sizeof(T)) + 32 * sizeof(T) + 16; }
 };
 
-template <class T, bool kPess, int kLogN>
+//
+// kExact (the float32 default for many-pick long columns, engine.cu
+// launch_sorted): after the sort, one thread walks the sorted gaps with the
+// reference's sequential `consumed` (omax.hpp:102-110) and one thread sums
+// V[row] * p in row order (omax.hpp:169-173), so the result is bit-identical
+// to robust_expectation; the parallel scan / tree sums below are skipped.
+template <class T, bool kPess, int kLogN, bool kExact = false>
 __global__ void __launch_bounds__(SortedShape<kLogN>::threads)
 omax_sorted(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
@@ -1214,6 +1220,41 @@ omax_sorted(int nlist, const int* __restrict__ list, const long long* __restrict
                 }
                 __syncthreads();
             }
+        }
+        if constexpr (kExact) {
+            // greedy along the sorted order, sequential as omaximize_sequential (omax.hpp:102-110):
+            // sgap[pos] becomes the extra share min(gap, avail) of every picked position
+            __shared__ int picks;
+            if (tid == 0) {
+                T consumed = T(0);
+                int j = 0;
+                for (; j < L; ++j) {
+                    const T avail = N_::sub(r, consumed);
+                    if (!(avail > T(0))) break;
+                    const int o = static_cast<int>(skey[j] & kPosMask);
+                    const T g = sgap[o];
+                    sgap[o] = g < avail ? g : avail;
+                    consumed = N_::add(consumed, g);
+                }
+                picks = j;
+            }
+            __syncthreads();
+            for (int j = picks + tid; j < L; j += NT) sgap[skey[j] & kPosMask] = T(-1); // not picked: p = lower
+            __syncthreads();
+            // products by position, then the row-order dot (omax.hpp:169-173) by one thread
+            T* prod = reinterpret_cast<T*>(skey);
+            for (int j = tid; j < L; j += NT) {
+                const T l = __ldg(lower + b + j), x = sgap[j];
+                prod[j] = N_::mul(__ldg(V + __ldg(rows + b + j)), x >= T(0) ? N_::add(l, x) : l);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                T dot = T(0);
+                for (int j = 0; j < L; ++j) dot = N_::add(dot, prod[j]);
+                q[c] = dot;
+            }
+            __syncthreads();
+            continue;
         }
         // prefix scan of the gaps in sorted order: thread tid owns sorted [tid*E, tid*E+E)
         int pos[E];

@@ -30,9 +30,9 @@ def host_state(s):
 def sampled_columns(rng):
     C = N * A
     cols = set(range(0, 16)) | set(range(C - 16, C))
-    for off in (2 ** 31, 2 ** 32, 3 * 2 ** 31):
+    for off in (2 ** 31, 2 ** 32, N * A * K - K):
         c = off // K
-        cols |= set(range(c - 12, c + 12))
+        cols |= set(range(max(0, c - 12), min(C, c + 12)))
     cols |= set(int(x) for x in rng.integers(0, C, 10_000))
     return sorted(cols)
 
