@@ -10,6 +10,7 @@
 #include "rimdp_b200.h"
 
 #include "generator.cuh"
+#include "omax_exact.cuh"
 #include "omax_kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -209,6 +210,7 @@ struct rimdp_model {
     cudaStream_t ls = nullptr;                // stream the next class launch goes to
     size_t l2_persist = 0;                    // bytes of L2 set aside for the value vector (0: none)
     bool pdl_now = false;                     // launches of the current iteration use PDL (launch_iteration)
+    DevBuf xs_gap, xs_pos, xs_val;            // exact_sort -> exact_dot scratch (float32 exact route), by store offset
     DevBuf vrange;                            // value_range slots [2][min, max] (order keys), for omax_bucket
     int vrange_parity = 0;
     const unsigned long long* vrange_cur = nullptr; // slot filled for the current launch_columns
@@ -765,7 +767,8 @@ void launch_sorted_class(rimdp_model* m, int count, const DevBuf& list, const T*
     }
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
     launch_pdl(m->pdl_now, k, blocks, Sh::threads, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
-                                                m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
+                                                m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, (const Ctl*)ctl,
+                                                (const int*)nullptr);
 }
 
 template <class T, bool P, int LG>
@@ -789,6 +792,16 @@ void launch_select_class(rimdp_model* m, int count, const int* list, const T* V,
                                               count_dev);
 }
 
+// Many-pick columns of a float32 model, bit-exact (omax_exact.cuh): the
+// bucket counting sort per column, then the sequential greedy and row-order
+// dot per column, then the bitonic exact kernel over the columns whose
+// buckets overflowed.
+struct FallbackSlots;
+FallbackSlots fallback_slots(rimdp_model* m, int cls, int count);
+
+template <class T, bool P, int LG>
+void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl);
+
 // Fallback list of one size class: [count A, count B, columns...].  The
 // bucket kernels count into one counter and clear the other, alternating
 // between launches, so no memset sits between the kernels of an iteration.
@@ -809,6 +822,54 @@ FallbackSlots fallback_slots(rimdp_model* m, int cls, int count) {
     FallbackSlots f{fbuf.as<int>() + 2, fbuf.as<int>() + par, fbuf.as<int>() + (par ^ 1)};
     par ^= 1;
     return f;
+}
+
+template <class T, bool P, int LG>
+void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
+    if constexpr (std::is_same<T, float>::value) {
+        using Sh = ExactShape<LG>;
+        auto ks = exact_sort<P, LG>;
+        static bool configured[64] = {};
+        static int per_sm[64] = {}, dot_per_sm[64] = {};
+        const int dev = m->device & 63;
+        if (!configured[dev]) {
+            CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem()));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], ks, Sh::NT, Sh::smem()));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dot_per_sm[dev], exact_dot, kExactDotWarps * 32, 0));
+            per_sm[dev] = std::max(per_sm[dev], 1);
+            dot_per_sm[dev] = std::max(dot_per_sm[dev], 1);
+            configured[dev] = true;
+        }
+        const size_t nz = (size_t)std::max<long long>(m->nnz, 1);
+        if (m->xs_gap.bytes < sizeof(float) * nz) {
+            m->xs_gap.ensure(sizeof(float) * nz);
+            m->xs_val.ensure(sizeof(float) * nz);
+            m->xs_pos.ensure(sizeof(unsigned short) * nz);
+        }
+        const FallbackSlots f = fallback_slots(m, LG - kSortedMinLog, count);
+        launch_pdl(m->pdl_now, ks, grid_for(count, 1, m->sm_count, per_sm[dev]), Sh::NT, Sh::smem(), m->ls, count,
+                   list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(), m->gap.as<float>(), V,
+                   m->xs_gap.as<float>(), m->xs_pos.as<unsigned short>(), m->xs_val.as<float>(), f.list, f.count,
+                   f.other, (const Ctl*)ctl);
+        launch_pdl(m->pdl_now, exact_dot, grid_for(count, kExactDotWarps, m->sm_count, dot_per_sm[dev]),
+                   kExactDotWarps * 32, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
+                   m->lower.as<float>(), m->rem.as<float>(), m->xs_gap.as<float>(),
+                   (const unsigned short*)m->xs_pos.as<unsigned short>(), (const float*)m->xs_val.as<float>(), q,
+                   (const Ctl*)ctl);
+        // overflowed columns: the bitonic exact kernel (after exact_dot, which wrote placeholders for them)
+        using SS = SortedShape<LG>;
+        auto kf = omax_sorted<float, P, LG, true>;
+        static bool fconf[64] = {};
+        if (!fconf[dev]) {
+            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::template smem<float>()));
+            fconf[dev] = true;
+        }
+        launch_pdl(m->pdl_now, kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
+                   (const int*)f.list, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(),
+                   m->gap.as<float>(), m->rem.as<float>(), V, q, (const Ctl*)ctl, (const int*)f.count);
+    } else {
+        launch_sorted_class<T, P, LG, true>(m, count, list, V, q, ctl);
+    }
 }
 
 // Columns of more than 256 entries: value-bucket kernel, then the selection
@@ -863,7 +924,7 @@ void launch_sorted(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* 
         const int i = LG - kSortedMinLog;
         if (L.n_sorted[i] > 0) {
             if (m->exact_sorted)
-                launch_sorted_class<T, P, LG, true>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+                launch_exact_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else if (m->bitonic)
                 launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else if (LG >= 9 && m->bucket)
@@ -1020,7 +1081,7 @@ void launch_sorted_fanout(rimdp_model* m, const ColumnLists& L, const T* V, T* q
         if (L.n_sorted[i] > 0) {
             f.pick();
             if (m->exact_sorted)
-                launch_sorted_class<T, P, LG, true>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
+                launch_exact_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else if (m->bitonic)
                 launch_sorted_class<T, P, LG>(m, L.n_sorted[i], L.sorted_list[i], V, q, ctl);
             else if (LG >= 9 && m->bucket)

@@ -1,0 +1,274 @@
+// Bit-exact many-pick long columns (33 .. 8192 entries) for float32 models.
+//
+// Why: at float32 one ulp of the values (1-2e-6 near 10-20) is of the order
+// of the stop tolerance (1e-6), so the stop test is met only at an exact
+// float32 fixed point and the iteration count depends on every rounding.  The
+// tree-order kernels (omax_bucket / omax_wbucket / omax_select) make the
+// reference's greedy decisions but sum in a different order; the kernels
+// below reproduce the reference's three sequential chains exactly:
+//   value_ordering (omax.hpp:41-58)        sort by (key(V[row]), position)
+//   omaximize_sequential (omax.hpp:98-112) consumed += gap along that order
+//   omax_expectation (omax.hpp:164-174)    dot += V[row] * p in row order
+//
+// Two passes per size class 2^LG:
+//
+//  exact_sort   one CTA per column.  The (key, position) sort is a counting
+//               sort over B = 2^LG equal-width buckets of the column's own
+//               key range (bucket index monotone in the key, so buckets are
+//               contiguous in the order and ties share a bucket), then each
+//               entry's rank inside its bucket is counted exactly against the
+//               bucket's other members (unique composite keys, any scatter
+//               order): O(L) work for spread-out values.  Writes, indexed by
+//               the column's store offset (global scratch, no host sizes):
+//                 S[sorted j]  = gap of the j-th entry in the order
+//                 POS[i]       = sorted position of entry i (row order)
+//                 VS[i]        = V[row_i]
+//               A column with a bucket of more than kExactMaxBucket entries
+//               (heavy ties / clustered values) goes to a fallback list for
+//               the bitonic omax_sorted<.., kExact = true>.
+//  exact_dot    one warp per column.  Lane 0 walks S sequentially (the
+//               reference's `consumed` chain) and turns every picked slot into
+//               its extra share min(gap, avail); then the warp forms the
+//               products V_i * (l_i + extra) of 32 row-order entries at a time
+//               (coalesced loads, the extra gathered by POS) into shared
+//               memory and lane 0 adds them sequentially.  Only the two
+//               dependent chains are serial; everything else is 32-wide.
+#pragma once
+
+#include "omax_kernels.cuh"
+
+namespace rimdp_dev {
+
+constexpr int kExactMaxBucket = 32;
+
+template <int LG>
+struct ExactShape {
+    static constexpr int N = 1 << LG;  // class capacity (and bucket count)
+    static constexpr int NT = N / 8 < 64 ? 64 : (N / 8 > 512 ? 512 : N / 8);
+    static constexpr int E = N / NT;   // entries per thread
+    static constexpr int NW = NT / 32;
+    static constexpr size_t smem() { return ((N + 1) * 4 + 15) / 16 * 16 + (size_t)N * 8; }
+};
+
+// Exclusive scan in place of cnt[0 .. NT*E), cnt[NT*E] = total.  Thread t owns
+// the E consecutive counters [t*E, t*E+E).  Contains two block barriers.
+template <int NT, int E>
+__device__ __forceinline__ void block_exclusive_scan(unsigned* cnt, unsigned* wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned v[E];
+    unsigned run = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        v[e] = cnt[tid * E + e];
+        run += v[e];
+    }
+    unsigned incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    unsigned base = incl - run;
+    for (int w = 0; w < wid; ++w) base += wsum[w];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        cnt[tid * E + e] = base;
+        base += v[e];
+    }
+    if (tid == NT - 1) cnt[NT * E] = base;
+    __syncthreads();
+}
+
+template <bool kPess, int LG>
+__global__ void __launch_bounds__(ExactShape<LG>::NT)
+exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+           const int* __restrict__ rows, const float* __restrict__ gap, const float* __restrict__ V,
+           float* __restrict__ S, unsigned short* __restrict__ POS, float* __restrict__ VS,
+           int* __restrict__ fb_list, int* __restrict__ fb_count, int* __restrict__ fb_other,
+           const Ctl* __restrict__ ctl) {
+    using Sh = ExactShape<LG>;
+    constexpr int N = Sh::N, NT = Sh::NT, E = Sh::E;
+    pdl_enter();
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) *fb_other = 0; // the other launch parity's count
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned* cnt = reinterpret_cast<unsigned*>(smem_raw);                                       // N + 1
+    unsigned long long* tmp = reinterpret_cast<unsigned long long*>(smem_raw + ((N + 1) * 4 + 15) / 16 * 16);
+    __shared__ unsigned kmin_s, kmax_s, wsum[32];
+    __shared__ int over;
+    const int tid = threadIdx.x;
+    for (int item = blockIdx.x; item < nlist; item += gridDim.x) {
+        const int c = list[item];
+        const long long b0 = colptr[c];
+        const int L = static_cast<int>(colptr[c + 1] - b0);
+        for (int k = tid; k <= N; k += NT) cnt[k] = 0u;
+        if (tid == 0) {
+            kmin_s = ~0u;
+            kmax_s = 0u;
+            over = 0;
+        }
+        __syncthreads();
+        unsigned key[E];
+        float g[E];
+        unsigned lmin = ~0u, lmax = 0u;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = tid + e * NT;
+            key[e] = ~0u;
+            g[e] = 0.f;
+            if (j < L) {
+                const float v = __ldg(V + __ldg(rows + b0 + j));
+                VS[b0 + j] = v;
+                g[e] = __ldg(gap + b0 + j);
+                key[e] = static_cast<unsigned>(order_key<float>(v, kPess));
+                lmin = key[e] < lmin ? key[e] : lmin;
+                lmax = key[e] > lmax ? key[e] : lmax;
+            }
+        }
+        lmin = __reduce_min_sync(kFull, lmin);
+        lmax = __reduce_max_sync(kFull, lmax);
+        if ((tid & 31) == 0) {
+            atomicMin(&kmin_s, lmin);
+            atomicMax(&kmax_s, lmax);
+        }
+        __syncthreads();
+        const unsigned kmin = kmin_s;
+        const unsigned long long span = static_cast<unsigned long long>(kmax_s - kmin) + 1ull;
+        int bk[E];
+        unsigned slot[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = tid + e * NT;
+            bk[e] = 0;
+            slot[e] = 0;
+            if (j < L) {
+                bk[e] = static_cast<int>((static_cast<unsigned long long>(key[e] - kmin) * N) / span);
+                slot[e] = atomicAdd(&cnt[bk[e]], 1u);
+            }
+        }
+        __syncthreads();
+        block_exclusive_scan<NT, E>(cnt, wsum);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = tid + e * NT;
+            if (j < L) tmp[cnt[bk[e]] + slot[e]] = (static_cast<unsigned long long>(key[e]) << 13) | j;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = tid + e * NT;
+            if (j < L) {
+                const unsigned s0 = cnt[bk[e]], s1 = cnt[bk[e] + 1];
+                if (s1 - s0 > static_cast<unsigned>(kExactMaxBucket)) {
+                    over = 1;
+                } else {
+                    const unsigned long long mine = (static_cast<unsigned long long>(key[e]) << 13) | j;
+                    unsigned r = 0;
+                    for (unsigned k = s0; k < s1; ++k) r += tmp[k] < mine;
+                    const unsigned sp = s0 + r;
+                    S[b0 + sp] = g[e];
+                    POS[b0 + j] = static_cast<unsigned short>(sp);
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && over) fb_list[atomicAdd(fb_count, 1)] = c;
+    }
+}
+
+constexpr int kExactDotWarps = 8;
+
+__global__ void __launch_bounds__(kExactDotWarps * 32)
+exact_dot(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+          const float* __restrict__ lower, const float* __restrict__ rem, float* __restrict__ S,
+          const unsigned short* __restrict__ POS, const float* __restrict__ VS, float* __restrict__ q,
+          const Ctl* __restrict__ ctl) {
+    using N_ = Num<float>;
+    pdl_enter();
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    __shared__ __align__(16) float buf[kExactDotWarps][128];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float* sb = buf[w];
+    for (int item = blockIdx.x * kExactDotWarps + w; item < nlist; item += gridDim.x * kExactDotWarps) {
+        const int c = list[item];
+        const long long b0 = colptr[c];
+        const int L = static_cast<int>(colptr[c + 1] - b0);
+        const float r = rem[c];
+        // ---- the greedy (omax.hpp:102-110) along the sorted gaps, 128 at a time ----
+        float consumed = 0.f;
+        int J = L;
+        for (int j0 = 0; j0 < L; j0 += 128) {
+            float gv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + u * 32 + lane;
+                gv[u] = j < L ? S[b0 + j] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sb[u * 32 + lane] = gv[u];
+            __syncwarp();
+            if (lane == 0) {
+                const int m = L - j0 < 128 ? L - j0 : 128;
+                int k = 0;
+                for (; k < m; ++k) {
+                    const float avail = N_::sub(r, consumed);
+                    if (!(avail > 0.f)) break;
+                    const float gk = sb[k];
+                    sb[k] = gk < avail ? gk : avail;
+                    consumed = N_::add(consumed, gk);
+                }
+                if (k < m) J = j0 + k;
+            }
+            __syncwarp();
+            J = __shfl_sync(kFull, J, 0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + u * 32 + lane;
+                if (j < J && j < L) S[b0 + j] = sb[u * 32 + lane];
+            }
+            __syncwarp();
+            if (J < L) break;
+        }
+        // ---- row-order expectation (omax.hpp:169-173) ----
+        float dot = 0.f;
+        for (int i0 = 0; i0 < L; i0 += 128) {
+            float x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * 32 + lane;
+                x[u] = 0.f;
+                if (i < L) {
+                    const int sp = POS[b0 + i];
+                    const float l = __ldg(lower + b0 + i);
+                    const float p = sp < J ? N_::add(l, S[b0 + sp]) : l;
+                    x[u] = N_::mul(VS[b0 + i], p);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sb[u * 32 + lane] = x[u];
+            __syncwarp();
+            if (lane == 0) {
+                const int m = L - i0 < 128 ? L - i0 : 128;
+                if (m == 128) {
+                    const float4* s4 = reinterpret_cast<const float4*>(sb);
+#pragma unroll 8
+                    for (int k = 0; k < 32; ++k) {
+                        const float4 v = s4[k];
+                        dot = N_::add(dot, v.x);
+                        dot = N_::add(dot, v.y);
+                        dot = N_::add(dot, v.z);
+                        dot = N_::add(dot, v.w);
+                    }
+                } else {
+                    for (int k = 0; k < m; ++k) dot = N_::add(dot, sb[k]);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) q[c] = dot;
+    }
+}
+
+} // namespace rimdp_dev

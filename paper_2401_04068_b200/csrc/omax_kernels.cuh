@@ -1139,7 +1139,8 @@ template <class T, bool kPess, int kLogN, bool kExact = false>
 __global__ void __launch_bounds__(SortedShape<kLogN>::threads)
 omax_sorted(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
-            const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl) {
+            const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl,
+            const int* __restrict__ count_dev = nullptr) {
     using N_ = Num<T>;
     using Bits = typename N_::Bits;
     using Sh = SortedShape<kLogN>;
@@ -1155,6 +1156,7 @@ omax_sorted(int nlist, const int* __restrict__ list, const long long* __restrict
     T* wsum = sgap + N;
     int& fix = *reinterpret_cast<int*>(wsum + 32);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (count_dev) nlist = *count_dev; // fallback list of exact_sort (omax_exact.cuh)
     for (int item = blockIdx.x; item < nlist; item += gridDim.x) {
         const int c = list[item];
         const long long b = colptr[c];

@@ -62,3 +62,32 @@ def test_c5_law_synthesis_matches_reference(name):
         assert sure.mean() > 0.5
         assert np.array_equal(policy.columns[sure], ref_pol[sure])
     m.close()
+
+
+def _ref_q(arrays, v, pess):
+    import oracle
+    sp, cp, rv, lo, up = arrays
+    return np.array([oracle.robust_expectation("ref", rv[cp[c]:cp[c + 1]], lo[cp[c]:cp[c + 1]], up[cp[c]:cp[c + 1]],
+                                               v, pess) for c in range(len(cp) - 1)], lo.dtype)
+
+
+@pytest.mark.parametrize("values", ["random", "ties", "levels"])
+@pytest.mark.parametrize("pess", [True, False])
+def test_f32_exact_route_columns_bit_exact(values, pess):
+    """Every float32 column class (1 .. 8192 entries, many picks) against the reference's robust_expectation,
+    bit for bit: spread-out values take exact_sort + exact_dot; heavy ties overflow the sort's buckets and
+    take the bitonic fallback."""
+    n = 9000
+    arrays = engine.generate_host(engine.gen_config(n, 1, law=1, alpha=0.9, kmax=8192, seed=21, dtype=np.float32))
+    rng = np.random.default_rng(5)
+    if values == "random":
+        v = rng.random(n).astype(np.float32)
+    elif values == "ties":
+        v = (rng.integers(0, 3, n) / 2.0).astype(np.float32)   # three values: every bucket overflows
+    else:
+        v = (rng.integers(0, 400, n) / 400.0).astype(np.float32)  # 400 levels: mixed
+    m = engine.DeviceModel.from_csc(*arrays)
+    q = m.column_values(v, pess)
+    ref = _ref_q(arrays, v, pess)
+    assert np.array_equal(bits(q), bits(ref)), np.flatnonzero(bits(q) != bits(ref))[:10]
+    m.close()
