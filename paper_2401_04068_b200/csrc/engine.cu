@@ -467,7 +467,10 @@ int column_class(long long len, double rem, double maxgap, int mode) {
     return kClassSorted + (lg - kSortedMinLog);
 }
 
-void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, const std::vector<signed char>& cls) {
+// by_length: sort each many-pick class list by decreasing length (longest first balances the persistent
+// grids of the float32 exact route)
+void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, const std::vector<signed char>& cls,
+                const long long* by_length = nullptr) {
     std::vector<int> sh, ex, md[2], ti[3], so[kSortedClasses];
     for (int c : cols) {
         const int k = cls[c];
@@ -490,6 +493,10 @@ void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, co
         upload_list(m, L.tiny_list[i], ti[i]);
     }
     for (int i = 0; i < kSortedClasses; ++i) {
+        if (by_length)
+            std::stable_sort(so[i].begin(), so[i].end(), [&](int a, int b) {
+                return by_length[a + 1] - by_length[a] > by_length[b + 1] - by_length[b];
+            });
         L.n_sorted[i] = (int)so[i].size();
         upload_list(m, L.sorted_list[i], so[i]);
     }
@@ -580,8 +587,9 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     // every column on the q path (the default: no fused short-state batches): the two sets of lists are the
     // same, so `all` is not built separately
     m->all_is_qp = qc.size() == allc.size();
-    if (!m->all_is_qp) fill_lists(m, m->all, allc, cls);
-    fill_lists(m, m->qp, qc, cls);
+    const long long* by_len = m->exact_sorted ? h_colptr : nullptr;
+    if (!m->all_is_qp) fill_lists(m, m->all, allc, cls, by_len);
+    fill_lists(m, m->qp, qc, cls, by_len);
     tr.mark("lists");
     m->nbatch = (int)bstates.size();
     m->nlong_states = (int)lstates.size();

@@ -29,10 +29,11 @@
 //  exact_dot    one warp per column.  Lane 0 walks S sequentially (the
 //               reference's `consumed` chain) and turns every picked slot into
 //               its extra share min(gap, avail); then the warp forms the
-//               products V_i * (l_i + extra) of 32 row-order entries at a time
+//               products V_i * (l_i + extra) of 128 row-order entries at a time
 //               (coalesced loads, the extra gathered by POS) into shared
-//               memory and lane 0 adds them sequentially.  Only the two
-//               dependent chains are serial; everything else is 32-wide.
+//               memory and lane 0 adds them sequentially, while the next
+//               chunk's loads are in flight.  Only the two dependent chains are
+//               serial; everything else is 32-wide.
 #pragma once
 
 #include "omax_kernels.cuh"
@@ -134,8 +135,14 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
             atomicMax(&kmax_s, lmax);
         }
         __syncthreads();
-        const unsigned kmin = kmin_s;
-        const unsigned long long span = static_cast<unsigned long long>(kmax_s - kmin) + 1ull;
+        // equal-width buckets over the column's value range, in adversary order (w = V pessimistic, -V
+        // optimistic): fl(w - w_min) * scale truncated is non-decreasing in w, so buckets are contiguous in
+        // the (key, position) order and equal values share one.  (Buckets over the order keys would not
+        // do: the keys of float values are logarithmic, so half of [0, 1) would land in 1/24 of them.)
+        const float vlo = value_of_key<float>(kmin_s, kPess), vhi = value_of_key<float>(kmax_s, kPess);
+        const float wmin = kPess ? vlo : -vlo, wmax = kPess ? vhi : -vhi;
+        const float width = __fsub_rn(wmax, wmin);
+        const float scale = width > 0.f && width < 3.0e38f ? __fdiv_rn(static_cast<float>(N), width) : 0.f;
         int bk[E];
         unsigned slot[E];
 #pragma unroll
@@ -144,7 +151,9 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
             bk[e] = 0;
             slot[e] = 0;
             if (j < L) {
-                bk[e] = static_cast<int>((static_cast<unsigned long long>(key[e] - kmin) * N) / span);
+                const float v = value_of_key<float>(key[e], kPess);
+                const float x = __fmul_rn(__fsub_rn(kPess ? v : -v, wmin), scale);
+                bk[e] = x < static_cast<float>(N - 1) ? static_cast<int>(x) : N - 1;
                 slot[e] = atomicAdd(&cnt[bk[e]], 1u);
             }
         }
@@ -180,6 +189,56 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
 
 constexpr int kExactDotWarps = 8;
 
+// Lane 0's share of the greedy over 128 sorted gaps staged in sb: four steps
+// per shared-memory vector load, the `consumed` chain as the only serial
+// dependency (a step after the stop only makes avail smaller, so the chain
+// runs unconditionally and `alive` decides what counts).  Returns the number
+// of picks in the chunk; sb[k] becomes min(gap_k, avail_k) for each pick.
+__device__ __forceinline__ int exact_walk_chunk(float* sb, int m, float r, float& consumed) {
+    using N_ = Num<float>;
+    float4* s4 = reinterpret_cast<float4*>(sb);
+    bool alive = true;
+    int picks = 0;
+    const int m4 = m & ~3;
+    float4 nxt = m4 > 0 ? s4[0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < m4; k += 4) {
+        const float4 gq = nxt;
+        if (k + 4 < m4) nxt = s4[(k >> 2) + 1];
+        float4 e;
+        float a = N_::sub(r, consumed);
+        alive = alive && a > 0.f;
+        picks += alive;
+        e.x = gq.x < a ? gq.x : a;
+        consumed = N_::add(consumed, gq.x);
+        a = N_::sub(r, consumed);
+        alive = alive && a > 0.f;
+        picks += alive;
+        e.y = gq.y < a ? gq.y : a;
+        consumed = N_::add(consumed, gq.y);
+        a = N_::sub(r, consumed);
+        alive = alive && a > 0.f;
+        picks += alive;
+        e.z = gq.z < a ? gq.z : a;
+        consumed = N_::add(consumed, gq.z);
+        a = N_::sub(r, consumed);
+        alive = alive && a > 0.f;
+        picks += alive;
+        e.w = gq.w < a ? gq.w : a;
+        consumed = N_::add(consumed, gq.w);
+        s4[k >> 2] = e;
+        if (!alive) return picks;
+    }
+    for (int k = m4; k < m; ++k) {
+        const float a = N_::sub(r, consumed);
+        if (!(a > 0.f)) return picks;
+        const float gk = sb[k];
+        sb[k] = gk < a ? gk : a;
+        consumed = N_::add(consumed, gk);
+        ++picks;
+    }
+    return picks;
+}
+
 __global__ void __launch_bounds__(kExactDotWarps * 32)
 exact_dot(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
           const float* __restrict__ lower, const float* __restrict__ rem, float* __restrict__ S,
@@ -197,73 +256,84 @@ exact_dot(int nlist, const int* __restrict__ list, const long long* __restrict__
         const int L = static_cast<int>(colptr[c + 1] - b0);
         const float r = rem[c];
         // ---- the greedy (omax.hpp:102-110) along the sorted gaps, 128 at a time ----
+        // lane k of the warp holds sorted entries k, k+32, k+64, k+96 of the chunk; the next chunk is
+        // loaded while lane 0 walks the current one
         float consumed = 0.f;
         int J = L;
-        for (int j0 = 0; j0 < L; j0 += 128) {
-            float gv[4];
+        float gv[4], gn[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = j0 + u * 32 + lane;
-                gv[u] = j < L ? S[b0 + j] : 0.f;
-            }
+        for (int u = 0; u < 4; ++u) {
+            const int j = u * 32 + lane;
+            gv[u] = j < L ? S[b0 + j] : 0.f;
+        }
+        for (int j0 = 0; j0 < L; j0 += 128) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) sb[u * 32 + lane] = gv[u];
-            __syncwarp();
-            if (lane == 0) {
-                const int m = L - j0 < 128 ? L - j0 : 128;
-                int k = 0;
-                for (; k < m; ++k) {
-                    const float avail = N_::sub(r, consumed);
-                    if (!(avail > 0.f)) break;
-                    const float gk = sb[k];
-                    sb[k] = gk < avail ? gk : avail;
-                    consumed = N_::add(consumed, gk);
-                }
-                if (k < m) J = j0 + k;
-            }
-            __syncwarp();
-            J = __shfl_sync(kFull, J, 0);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int j = j0 + u * 32 + lane;
-                if (j < J && j < L) S[b0 + j] = sb[u * 32 + lane];
+                const int j = j0 + 128 + u * 32 + lane;
+                gn[u] = j < L ? S[b0 + j] : 0.f;
             }
             __syncwarp();
-            if (J < L) break;
+            int picks = 0;
+            const int m = L - j0 < 128 ? L - j0 : 128;
+            if (lane == 0) picks = exact_walk_chunk(sb, m, r, consumed);
+            picks = __shfl_sync(kFull, picks, 0);
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = u * 32 + lane;
+                if (k < picks) S[b0 + j0 + k] = sb[k];
+                gv[u] = gn[u];
+            }
+            __syncwarp();
+            if (picks < m) {
+                J = j0 + picks;
+                break;
+            }
         }
-        // ---- row-order expectation (omax.hpp:169-173) ----
+        // ---- row-order expectation (omax.hpp:169-173), 128 products at a time ----
         float dot = 0.f;
+        int sp[4];
+        float lw[4], vw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = u * 32 + lane;
+            sp[u] = i < L ? POS[b0 + i] : 0x7fffffff;
+            lw[u] = i < L ? __ldg(lower + b0 + i) : 0.f;
+            vw[u] = i < L ? VS[b0 + i] : 0.f;
+        }
         for (int i0 = 0; i0 < L; i0 += 128) {
+            float ex[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ex[u] = sp[u] < J ? S[b0 + sp[u]] : 0.f;
             float x[4];
 #pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = N_::mul(vw[u], sp[u] < J ? N_::add(lw[u], ex[u]) : lw[u]);
+            // the next chunk's row-order data is in flight during the serial sum
+#pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int i = i0 + u * 32 + lane;
-                x[u] = 0.f;
-                if (i < L) {
-                    const int sp = POS[b0 + i];
-                    const float l = __ldg(lower + b0 + i);
-                    const float p = sp < J ? N_::add(l, S[b0 + sp]) : l;
-                    x[u] = N_::mul(VS[b0 + i], p);
-                }
+                const int i = i0 + 128 + u * 32 + lane;
+                sp[u] = i < L ? POS[b0 + i] : 0x7fffffff;
+                lw[u] = i < L ? __ldg(lower + b0 + i) : 0.f;
+                vw[u] = i < L ? VS[b0 + i] : 0.f;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) sb[u * 32 + lane] = x[u];
             __syncwarp();
             if (lane == 0) {
                 const int m = L - i0 < 128 ? L - i0 : 128;
-                if (m == 128) {
-                    const float4* s4 = reinterpret_cast<const float4*>(sb);
+                const float4* s4 = reinterpret_cast<const float4*>(sb);
+                const int m4 = m >> 2;
 #pragma unroll 8
-                    for (int k = 0; k < 32; ++k) {
-                        const float4 v = s4[k];
-                        dot = N_::add(dot, v.x);
-                        dot = N_::add(dot, v.y);
-                        dot = N_::add(dot, v.z);
-                        dot = N_::add(dot, v.w);
-                    }
-                } else {
-                    for (int k = 0; k < m; ++k) dot = N_::add(dot, sb[k]);
+                for (int k = 0; k < m4; ++k) {
+                    const float4 v = s4[k];
+                    dot = N_::add(dot, v.x);
+                    dot = N_::add(dot, v.y);
+                    dot = N_::add(dot, v.z);
+                    dot = N_::add(dot, v.w);
                 }
+                for (int k = m4 * 4; k < m; ++k) dot = N_::add(dot, sb[k]);
             }
             __syncwarp();
         }
