@@ -238,11 +238,20 @@ def engine_arm(args, w):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RIMDP_BENCH_DEVICE_MAP=0,0 (tests on a one-GPU box): local rank r runs on device map[r]
+    dmap = os.environ.get("RIMDP_BENCH_DEVICE_MAP")
+    if dmap:
+        local = int(dmap.split(",")[local])
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # control plane only (IPC handle swap, barriers, max over ranks): gloo on host tensors.  The peer
+        # exchange needs no collective library; the NCCL baseline needs NCCL for its all-gather.
+        if args.exchange == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dtype = np.float64 if args.dtype == "f64" else np.float32
     es = np.dtype(dtype).itemsize
     n = w["states"]
@@ -250,7 +259,7 @@ def engine_arm(args, w):
     local_nnz = m.nnz
     total_nnz = local_nnz
     if world > 1:
-        t = torch.tensor([local_nnz, local_nnz], dtype=torch.int64, device="cuda")
+        t = torch.tensor([local_nnz, local_nnz], dtype=torch.int64, device="cuda" if args.exchange == "nccl" else "cpu")
         dist.all_reduce(t[:1], op=dist.ReduceOp.SUM)
         dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
         total_nnz, max_nnz = int(t[0]), int(t[1])
@@ -276,21 +285,19 @@ def engine_arm(args, w):
         k_done, _, _ = m.poll()
         assert k_done == total, (k_done, total)
     else:
-        shard = sharded.DeviceShard(m, rank, world, n)
-        solver = sharded.ShardedSolver(shard)
+        # the state-sharded solve: V exchanged by the action kernel's peer stores (sharded.PeerShard), or
+        # the unfused NCCL all-gather baseline with --exchange nccl
+        shard = (sharded.PeerShard if args.exchange == "peer" else sharded.NcclShard)(m, rank, world, n)
         shard.begin(**run_kw)
-        with shard.stream_context():
-            for k in range(1, args.warmup + 1):
-                solver.enqueue(k)
+        shard.advance(args.warmup)
+        shard.poll()
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
         clk.mark("timed")
-        with shard.stream_context():
-            start.record(stream)
-            for k in range(args.warmup + 1, total + 1):
-                solver.enqueue(k)
-            end.record(stream)
+        start.record(stream)
+        shard.advance(args.steps)
+        end.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
         k_done, _, _ = shard.poll()
@@ -299,19 +306,25 @@ def engine_arm(args, w):
     clk.mark("end")
     ms = start.elapsed_time(end)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if args.exchange == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
 
     # ---- dominant kernels: the column phase, event-timed per launch ------
-    m.begin(**run_kw)
+    if world > 1:
+        shard.begin(**run_kw)  # includes the barrier after the windows are reset
+    else:
+        m.begin(**run_kw)
     m.advance(args.warmup)
     m.poll()
     m.profile(True)
     m.profile_read()
     prof_iters = min(args.steps, 200)
-    m.advance(prof_iters)
+    if world > 1 and args.exchange == "nccl":
+        shard.advance(prof_iters)
+    else:
+        m.advance(prof_iters)
     fused_ms, cols_ms, act_ms, it, kpi = m.profile_read()
     m.profile(False)
     m.finish()
@@ -363,11 +376,13 @@ def engine_arm(args, w):
             h2d += sum(a.nbytes for a in parts)
         else:
             dm = m
-        res = sharded.ShardedSolver(sharded.DeviceShard(dm, rank, world, n)).solve(finite=False, **kw)
+        sh = (sharded.PeerShard if args.exchange == "peer" else sharded.NcclShard)(dm, rank, world, n) \
+            if dm is not m else shard
+        res = sharded.ShardedSolver(sh).solve(finite=False, **kw)
         e2e_iters, values, residual = res.iterations, res.values, res.residual
     e2e_s = time.perf_counter() - t
     if world > 1:
-        tt = torch.tensor([e2e_s], device="cuda")
+        tt = torch.tensor([e2e_s], device="cuda" if args.exchange == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     d2h = values.nbytes + residual.nbytes
@@ -402,8 +417,9 @@ def engine_arm(args, w):
         "dtype": args.dtype,
         "data": data_desc(w) + ("; generated on host, resident in HBM" if w["source"] == "reference" else
                                 "; generated directly in HBM"),
-        "config": config_for(w, total_nnz, es, f"state-sharded x{world} (peer exchange of V)" if world > 1
-                             else "single GPU"),
+        "config": config_for(w, total_nnz, es, (f"state-sharded x{world}, V exchanged by "
+                                                + ("fused peer stores (CUDA IPC, NVLink)" if args.exchange == "peer"
+                                                   else "NCCL all-gather")) if world > 1 else "single GPU"),
         "scheduler": {"short_columns": info.short_columns, "exact_long_columns": info.mid_columns,
                       "sorted_long_columns": info.long_columns, "max_column_length": info.max_column_length},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -419,9 +435,11 @@ def engine_arm(args, w):
                 "reference_iterations": ref_iters, "values_bit_exact_vs_reference": bit_exact,
                 "max_abs_diff_vs_reference_samples": sample_diff,
                 "call": ("DeviceModel.from_csc + problems.value_iteration (C ABI)" if world == 1 else
-                         "DeviceModel.from_csc_shard + sharded.ShardedSolver.solve (C ABI + NCCL)")},
+                         "DeviceModel.from_csc_shard + sharded.ShardedSolver.solve (C ABI; V exchanged "
+                         + ("by the action kernel's peer stores over CUDA IPC)" if args.exchange == "peer" else
+                            "by NCCL all-gather)"))},
         "time_to_convergence_s": e2e_s,
-        "gpu_launches": args.steps * (kpi + (1 if world > 1 else 0)),
+        "gpu_launches": args.steps * kpi,  # kernels_per_iteration counts peer_sync_stop when sharded
         "clocks": clk.summary(),
     }
     if world > 1:
@@ -554,6 +572,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU reference work")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="experiments: skip the end-to-end solve (no e2e number)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: V exchange of the sharded solve (fused peer stores, or the NCCL baseline)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak (C2 law, N x the states) or strong (fixed model)")
     args = ap.parse_args()

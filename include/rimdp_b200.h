@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define RIMDP_B200_ABI_VERSION 3
+#define RIMDP_B200_ABI_VERSION 4
 
 /* Scalar type of a model: NumericTraits<double|float> (numeric.hpp:53-81).
  * The exact Rational instantiation (numeric.hpp:83-101) has no device path. */
@@ -240,6 +240,45 @@ int rimdp_solve_residual_slots(rimdp_model* model, void** slots);
  * max |V_k - V_{k-1}| is then taken over the whole value vector on the
  * device, so no collective is needed for it. */
 int rimdp_solve_stop_test(rimdp_model* model);
+
+/* ---- multi-GPU: peer exchange of a state-sharded solve -----
+ * New: the reference has no multi-device path (its only parallelism is the
+ * per-state fork/join of parallel.hpp:56-64 inside bellman.hpp:88-115).
+ * Every shard owns an exchange window in its HBM (the double-buffered value
+ * vector, per-rank residual slots and iteration flags).  Each iteration the
+ * action kernel stores every new value of the shard's states into every
+ * peer's window over NVLink (CUDA IPC or peer access) as it computes them, and
+ * publishes its residual and a flag with system-scope release; a one-warp
+ * kernel then waits for all ranks' flags and runs the stop test on the
+ * maximum published residual (identical on every rank).  No collective
+ * library call, no host synchronisation per iteration.
+ *
+ * Multi-process (one process per GPU): call rimdp_model_set_value_capacity
+ * (same value on every rank, >= the global state count), export the window's
+ * 64-byte CUDA IPC handle, exchange the handles (e.g. torch.distributed
+ * all_gather_object), connect.  Then per solve: rimdp_solve_begin with
+ * external_stop = 1 on every rank, a barrier across ranks (the windows are
+ * reset by begin), then rimdp_solve_advance / _poll / _finish as usual. */
+#define RIMDP_MAX_WORLD 8
+int rimdp_exchange_export(rimdp_model* model, void* ipc_handle_out /* 64 bytes, may be NULL */);
+int rimdp_exchange_connect(rimdp_model* model, int32_t rank, int32_t world,
+                           const void* ipc_handles /* world x 64 bytes, rank order */);
+/* Single process, several shards (devices may repeat: shards sharing a GPU). */
+int rimdp_exchange_connect_local(rimdp_model* const* shards, int32_t world);
+
+/* Single process, several devices: the model cut into `world` contiguous
+ * state ranges of equal transition counts (one shard per entry of `devices`,
+ * NULL = 0 .. world-1; a device may repeat), connected as above.  solve has
+ * rimdp_solve's contract on the whole model: global column indices in
+ * plan.forced and out.chosen, V and residual of all states; results are
+ * bit-identical to a one-device solve (sharding changes no per-state
+ * arithmetic). */
+typedef struct rimdp_multi rimdp_multi;
+int rimdp_multi_create(const rimdp_model_desc* desc, int32_t world, const int32_t* devices, rimdp_multi** out);
+int rimdp_multi_solve(rimdp_multi* multi, const rimdp_plan* plan, const rimdp_outputs* out);
+/* world, state_begin[world + 1] (the cut), devices[world]; any may be NULL. */
+int rimdp_multi_info(rimdp_multi* multi, int32_t* world, int32_t* state_begin, int32_t* devices);
+int rimdp_multi_destroy(rimdp_multi* multi);
 
 /* One Bellman step from `v_in` (bellman.hpp:127-133, with the optional
  * forced column per state of bellman_step_impl, :96-101). */

@@ -151,6 +151,7 @@ struct Infeasible {
 
 struct SolveState {
     DevBuf v[2], q, chosen, frozen, rewards, forced, res, ctl, work;
+    void* vb[2] = {nullptr, nullptr}; // the value double buffer of the solve: v[0..1], or the exchange window
     bool has_frozen = false, has_rewards = false, has_forced = false;
     int forced_td = 0;
     int pess = 1, maxi = 1, finite = 1;
@@ -215,6 +216,22 @@ struct rimdp_model {
     int vrange_parity = 0;
     const unsigned long long* vrange_cur = nullptr; // slot filled for the current launch_columns
     SolveState s;
+    // peer exchange of a state-sharded solve (rimdp_exchange_*): this shard's window (cudaMalloc, IPC
+    // exportable) = [V buffer 0 | V buffer 1 | residual slots [2][kMaxWorld] | flags [kMaxWorld]]
+    struct Exchange {
+        void* win = nullptr;
+        size_t vbytes = 0;               // bytes of one value buffer (capacity x element, 256-aligned)
+        long long cap = 0;               // value buffer capacity in entries
+        bool connected = false;
+        bool shared_device = false;      // some peer window lives on this shard's device (tests on one GPU)
+        int world = 1, rank = 0;
+        std::vector<void*> opened;       // IPC-opened peer windows
+        DevBuf table;                    // PeerTable
+        unsigned long long* res() const { return reinterpret_cast<unsigned long long*>(static_cast<char*>(win) + 2 * vbytes); }
+        unsigned long long* flags() const { return res() + 2 * kMaxWorld; }
+        static size_t tail() { return 3 * kMaxWorld * sizeof(unsigned long long); }
+    } x;
+    int col_offset = 0;                       // multi-GPU shard: global index of local column 0 (error reports)
 };
 
 namespace {
@@ -710,13 +727,24 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     s.max_iterations = p->max_iterations;
     s.eps = p->eps;
     s.discount = p->discount;
-    const long long cap = std::max<long long>(N, m->value_capacity);
-    s.v[0].ensure(sizeof(T) * cap);
-    s.v[1].ensure(sizeof(T) * cap);
+    long long cap = std::max<long long>(N, m->value_capacity);
+    if (m->x.connected) {
+        // the exchange window holds the double buffer; its residual slots and flags restart at 0 (the driver
+        // synchronises all ranks after begin, before any rank enqueues iteration 1)
+        cap = m->x.cap;
+        s.vb[0] = m->x.win;
+        s.vb[1] = static_cast<char*>(m->x.win) + m->x.vbytes;
+        CK(cudaMemsetAsync(m->x.res(), 0, rimdp_model::Exchange::tail(), m->stream));
+    } else {
+        s.v[0].ensure(sizeof(T) * cap);
+        s.v[1].ensure(sizeof(T) * cap);
+        s.vb[0] = s.v[0].p;
+        s.vb[1] = s.v[1].p;
+    }
     setup_l2_persistence(m, sizeof(T) * (size_t)N);
     if (cap > N) {
-        CK(cudaMemsetAsync(s.v[0].as<T>() + N, 0, sizeof(T) * (cap - N), m->stream));
-        CK(cudaMemsetAsync(s.v[1].as<T>() + N, 0, sizeof(T) * (cap - N), m->stream));
+        CK(cudaMemsetAsync(static_cast<T*>(s.vb[0]) + N, 0, sizeof(T) * (cap - N), m->stream));
+        CK(cudaMemsetAsync(static_cast<T*>(s.vb[1]) + N, 0, sizeof(T) * (cap - N), m->stream));
     }
     s.q.ensure(sizeof(T) * std::max(1, m->ncols));
     s.res.ensure(sizeof(T) * N);
@@ -725,8 +753,8 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
         fail(RIMDP_ERR_INVALID_ARGUMENT, "plan.initial is required");
         throw Fail{RIMDP_ERR_INVALID_ARGUMENT};
     }
-    CK(cudaMemcpyAsync(s.v[0].p, p->initial, sizeof(T) * N, cudaMemcpyHostToDevice, m->stream));
-    CK(cudaMemcpyAsync(s.v[1].p, s.v[0].p, sizeof(T) * N, cudaMemcpyDeviceToDevice, m->stream));
+    CK(cudaMemcpyAsync(s.vb[0], p->initial, sizeof(T) * N, cudaMemcpyHostToDevice, m->stream));
+    CK(cudaMemcpyAsync(s.vb[1], s.vb[0], sizeof(T) * N, cudaMemcpyDeviceToDevice, m->stream));
     s.has_frozen = p->frozen != nullptr;
     s.host_frozen_copy.clear();
     if (s.has_frozen) {
@@ -756,7 +784,7 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     CK(cudaMemsetAsync(s.work.p, 0, 2 * kWorkKinds * sizeof(unsigned), m->stream));
     s.launched = 0;
     s.active = true;
-    s.record_only = p->external_stop != 0;
+    s.record_only = p->external_stop != 0 || m->x.connected; // sharded: the stop test is global
 }
 
 template <class T, bool P, int LG, bool X = false>
@@ -1167,8 +1195,8 @@ constexpr int kPdlMaxKernels = 3;
 template <class T>
 void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     SolveState& s = m->s;
-    const T* vin = s.v[(k - 1) & 1].as<T>();
-    T* vout = s.v[k & 1].as<T>();
+    const T* vin = static_cast<const T*>(s.vb[(k - 1) & 1]);
+    T* vout = static_cast<T*>(s.vb[k & 1]);
     Ctl* ctl = s.ctl.as<Ctl>();
     unsigned* work = s.work.as<unsigned>() + (k & 1) * kWorkKinds;
     cudaEvent_t* ev = nullptr;
@@ -1198,8 +1226,12 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     a.k = k;
     a.record_only = s.record_only;
     a.work = s.work.as<unsigned>();
+    a.peers = m->x.connected ? m->x.table.as<PeerTable>() : nullptr;
     const T* rw = s.has_rewards ? s.rewards.as<T>() : nullptr;
-    m->pdl_now = kernels_per_iteration(m) <= kPdlMaxKernels && !m->l2_persist && m->nstreams == 1;
+    // PDL lets the next kernel's blocks become resident early; with two shards on one device (tests) those
+    // blocks could take the SMs the other shard needs to publish the flag this shard waits for
+    m->pdl_now = kernels_per_iteration(m) <= kPdlMaxKernels && !m->l2_persist && m->nstreams == 1 &&
+                 !(m->x.connected && m->x.shared_device);
     if (m->nbatch > 0) {
         a.finalize = m->nlong_states == 0;
         // occupancy variant: 4 resident blocks (64 registers) or 5 (48 registers)
@@ -1223,6 +1255,11 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
         launch_pdl(m->pdl_now, action_reduce<T>, grid_for(m->nlong_states, 256, m->sm_count, 8), 256, 0, m->stream,
             a, m->nlong_states, m->long_states.as<int>(), s.q.as<T>(), vin, vout, rw, (T)s.discount, (T)s.eps, ctl);
     }
+    if (m->x.connected) {
+        // the global stop test once every rank has published iteration k (peer_sync_stop)
+        peer_sync_stop<T><<<1, 32, 0, m->stream>>>(ctl, m->x.table.as<PeerTable>(), k, s.finite, s.horizon,
+                                                   std::max(1LL, s.max_iterations), (T)s.eps);
+    }
     if (ev) CK(cudaEventRecord(ev[3], m->stream));
     m->pdl_now = false;
     CK(cudaGetLastError());
@@ -1233,13 +1270,14 @@ int kernels_per_iteration(const rimdp_model* m) {
             (m->qp.n_medium[0] > 0) + (m->qp.n_medium[1] > 0) + (m->qp.n_tiny[0] > 0) + (m->qp.n_tiny[1] > 0) +
             (m->qp.n_tiny[2] > 0);
     for (int i = 0; i < kSortedClasses; ++i) k += m->qp.n_sorted[i] > 0;
-    return k;
+    return k + (m->x.connected ? 1 : 0);
 }
 
 // First infeasible column that a step would evaluate (bellman.hpp:88-112:
 // frozen states are skipped, forced states evaluate one column; the lowest
 // state index wins, parallel.hpp:41-67).
-const Infeasible* first_evaluated_infeasible(rimdp_model* m, const rimdp_plan* p) {
+// only_it >= 0: only iteration only_it + 1's row (multi-GPU solves scan the rows across shards in order)
+const Infeasible* first_evaluated_infeasible(rimdp_model* m, const rimdp_plan* p, long long only_it = -1) {
     if (m->infeasible_cols.empty()) return nullptr;
     std::vector<char> bad(m->ncols, 0);
     for (const auto& f : m->infeasible_cols) bad[f.col] = 1;
@@ -1251,7 +1289,7 @@ const Infeasible* first_evaluated_infeasible(rimdp_model* m, const rimdp_plan* p
     };
     const long long rows = (p->forced && p->forced_time_dependent) ? std::max<long long>(p->horizon, 1) : 1;
     // iteration k = 1 uses row horizon - 1, k = 2 row horizon - 2, ...
-    for (long long it = 0; it < rows; ++it) {
+    for (long long it = only_it >= 0 ? only_it : 0; it < (only_it >= 0 ? std::min(rows, only_it + 1) : rows); ++it) {
         const long long t = (p->forced && p->forced_time_dependent) ? p->horizon - 1 - it : 0;
         for (int s = 0; s < n; ++s) {
             if (p->frozen && p->frozen[m->state_begin + s]) continue;
@@ -1270,7 +1308,7 @@ const Infeasible* first_evaluated_infeasible(rimdp_model* m, const rimdp_plan* p
     return nullptr;
 }
 
-int report_infeasible(const Infeasible* f, rimdp_dtype dtype) {
+int report_infeasible(const Infeasible* f, rimdp_dtype dtype, int col_offset = 0) {
     char num[64];
     // shortest round-trip text, as NumericTraits::to_string (numeric.hpp:30-35)
     for (int prec = 1; prec <= 17; ++prec) {
@@ -1280,7 +1318,7 @@ int report_infeasible(const Infeasible* f, rimdp_dtype dtype) {
     }
     fail(RIMDP_ERR_INFEASIBLE_COLUMN, "InfeasibleColumn: %s bounds sum to %s %s", f->kind == 1 ? "lower" : "upper",
          num, f->kind == 1 ? "> 1" : "< 1");
-    g_err_info.column = f->col;
+    g_err_info.column = f->col + col_offset;
     g_err_info.infeasible_kind = f->kind;
     g_err_info.infeasible_sum = f->sum;
     return RIMDP_ERR_INFEASIBLE_COLUMN;
@@ -1322,13 +1360,13 @@ void finish_t(rimdp_model* m, const rimdp_outputs* o, long long k) {
     SolveState& s = m->s;
     const int N = m->n_global;
     if (o->values)
-        CK(cudaMemcpyAsync(o->values, s.v[k & 1].p, sizeof(T) * N, cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaMemcpyAsync(o->values, s.vb[k & 1], sizeof(T) * N, cudaMemcpyDeviceToHost, m->stream));
     if (o->residual) {
         if (k == 0) {
             CK(cudaMemsetAsync(s.res.p, 0, sizeof(T) * N, m->stream));
         } else {
-            residual_vector<T><<<grid_for(N, 256, m->sm_count, 8), 256, 0, m->stream>>>(N, s.v[k & 1].as<T>(),
-                                                                                        s.v[(k - 1) & 1].as<T>(),
+            residual_vector<T><<<grid_for(N, 256, m->sm_count, 8), 256, 0, m->stream>>>(N, static_cast<T*>(s.vb[k & 1]),
+                                                                                        static_cast<T*>(s.vb[(k - 1) & 1]),
                                                                                         s.res.as<T>());
             CK(cudaGetLastError());
         }
@@ -1406,7 +1444,7 @@ int solve_t(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
             advance_t<T>(m, 1);
             c = read_ctl(m);
             k = c.k;
-            CK(cudaMemcpy(hv.data(), m->s.v[k & 1].p, sizeof(T) * m->n_global, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(hv.data(), m->s.vb[k & 1], sizeof(T) * m->n_global, cudaMemcpyDeviceToHost));
             o->on_iteration(k, hv.data(), o->user);
             if (c.done) break;
         }
@@ -1592,6 +1630,9 @@ int rimdp_model_destroy(rimdp_model* m) {
             if (m->join_ev[i]) cudaEventDestroy(m->join_ev[i]);
         }
         if (m->fork_ev) cudaEventDestroy(m->fork_ev);
+        for (void* w : m->x.opened) cudaIpcCloseMemHandle(w);
+        m->x.table.release();
+        if (m->x.win) cudaFree(m->x.win);
         if (m->stream) cudaStreamDestroy(m->stream);
         m->stream = nullptr;
     }
@@ -1754,11 +1795,11 @@ int rimdp_solve_stop_test(rimdp_model* m) {
         const int blocks = grid_for(m->n_global, 256, m->sm_count, 4);
         if (m->dtype == RIMDP_F64)
             global_stop_test<double><<<blocks, 256, 0, m->stream>>>(
-                m->n_global, s.v[k & 1].as<double>(), s.v[(k - 1) & 1].as<double>(), s.ctl.as<Ctl>(), k, s.finite,
+                m->n_global, static_cast<double*>(s.vb[k & 1]), static_cast<double*>(s.vb[(k - 1) & 1]), s.ctl.as<Ctl>(), k, s.finite,
                 s.horizon, s.max_iterations, (double)s.eps);
         else
             global_stop_test<float><<<blocks, 256, 0, m->stream>>>(
-                m->n_global, s.v[k & 1].as<float>(), s.v[(k - 1) & 1].as<float>(), s.ctl.as<Ctl>(), k, s.finite,
+                m->n_global, static_cast<float*>(s.vb[k & 1]), static_cast<float*>(s.vb[(k - 1) & 1]), s.ctl.as<Ctl>(), k, s.finite,
                 s.horizon, s.max_iterations, (float)s.eps);
         CK(cudaGetLastError());
         return RIMDP_OK;
@@ -1771,10 +1812,138 @@ int rimdp_model_set_value_capacity(rimdp_model* m, int64_t entries) {
     return RIMDP_OK;
 }
 
+// ---- peer exchange (state-sharded solves) ----------
+
+static int exchange_alloc(rimdp_model* m) {
+    if (m->x.win) return RIMDP_OK;
+    const size_t es = elem_size(m->dtype);
+    m->x.cap = std::max<long long>(m->n_global, m->value_capacity);
+    m->x.vbytes = ((size_t)m->x.cap * es + 255) / 256 * 256;
+    const size_t bytes = 2 * m->x.vbytes + rimdp_model::Exchange::tail();
+    CK(cudaMalloc(&m->x.win, bytes)); // plain cudaMalloc: IPC-exportable, unlike the stream-ordered pool
+    CK(cudaMemset(m->x.win, 0, bytes));
+    return RIMDP_OK;
+}
+
+// Builds and uploads the PeerTable from the ranks' window base pointers (in this process's address space).
+static void exchange_table(rimdp_model* m, int rank, int world, const std::vector<char*>& bases,
+                           const std::vector<size_t>& vbytes) {
+    PeerTable t{};
+    t.world = world;
+    t.rank = rank;
+    for (int p = 0; p < world; ++p) {
+        t.v[p][0] = bases[p];
+        t.v[p][1] = bases[p] + vbytes[p];
+        t.res[p] = reinterpret_cast<unsigned long long*>(bases[p] + 2 * vbytes[p]);
+        t.flag[p] = t.res[p] + 2 * kMaxWorld;
+    }
+    m->x.table.ensure(sizeof(PeerTable));
+    CK(cudaMemcpy(m->x.table.p, &t, sizeof t, cudaMemcpyHostToDevice));
+    m->x.world = world;
+    m->x.rank = rank;
+    m->x.connected = true;
+}
+
+static int check_exchange(rimdp_model* m, int rank, int world) {
+    if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "rank %d / world %d outside 1..%d", rank, world, kMaxWorld);
+    if (m->nbatch > 0)
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "the fused short-state path (RIMDP_FUSED) has no peer exchange");
+    if (m->s.active) return fail(RIMDP_ERR_INVALID_ARGUMENT, "a solve is active");
+    return RIMDP_OK;
+}
+
+int rimdp_exchange_export(rimdp_model* m, void* handle_out) {
+    if (!m) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null model");
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        exchange_alloc(m);
+        if (handle_out) {
+            cudaIpcMemHandle_t h;
+            CK(cudaIpcGetMemHandle(&h, m->x.win));
+            std::memcpy(handle_out, &h, sizeof h);
+        }
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_exchange_connect(rimdp_model* m, int32_t rank, int32_t world, const void* handles) {
+    if (!m || !handles) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    if (int st = check_exchange(m, rank, world)) return st;
+    return guarded([&]() -> int {
+        DeviceGuard g(m->device);
+        exchange_alloc(m);
+        const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+        std::vector<char*> bases(world);
+        std::vector<size_t> vb(world, m->x.vbytes); // every rank sizes its window for the same capacity
+        for (void* w : m->x.opened) cudaIpcCloseMemHandle(w);
+        m->x.opened.clear();
+        m->x.shared_device = false;
+        for (int p = 0; p < world; ++p) {
+            if (p == rank) {
+                bases[p] = static_cast<char*>(m->x.win);
+                continue;
+            }
+            void* ptr = nullptr;
+            CK(cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess));
+            m->x.opened.push_back(ptr);
+            bases[p] = static_cast<char*>(ptr);
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.device == m->device) m->x.shared_device = true;
+        }
+        exchange_table(m, rank, world, bases, vb);
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_exchange_connect_local(rimdp_model* const* shards, int32_t world) {
+    if (!shards || world < 1) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    for (int r = 0; r < world; ++r) {
+        if (!shards[r]) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null shard %d", r);
+        if (int st = check_exchange(shards[r], r, world)) return st;
+        if (shards[r]->dtype != shards[0]->dtype || shards[r]->n_global != shards[0]->n_global)
+            return fail(RIMDP_ERR_INVALID_ARGUMENT, "shard %d does not belong to the same model", r);
+    }
+    return guarded([&]() -> int {
+        std::vector<char*> bases(world);
+        std::vector<size_t> vb(world);
+        for (int r = 0; r < world; ++r) {
+            DeviceGuard g(shards[r]->device);
+            exchange_alloc(shards[r]);
+            bases[r] = static_cast<char*>(shards[r]->x.win);
+            vb[r] = shards[r]->x.vbytes;
+        }
+        for (int r = 0; r < world; ++r) {
+            DeviceGuard g(shards[r]->device);
+            bool shared = false;
+            for (int p = 0; p < world; ++p) {
+                if (p == r) continue;
+                if (shards[p]->device == shards[r]->device) {
+                    shared = true;
+                } else {
+                    int can = 0;
+                    CK(cudaDeviceCanAccessPeer(&can, shards[r]->device, shards[p]->device));
+                    if (!can) {
+                        fail(RIMDP_ERR_CUDA, "device %d cannot access device %d (no P2P)", shards[r]->device,
+                             shards[p]->device);
+                        throw Fail{RIMDP_ERR_CUDA};
+                    }
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(shards[p]->device, 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                    cudaGetLastError();
+                }
+            }
+            shards[r]->x.shared_device = shared;
+            exchange_table(shards[r], r, world, bases, vb);
+        }
+        return RIMDP_OK;
+    });
+}
+
 int rimdp_solve_value_buffers(rimdp_model* m, void** b0, void** b1) {
     if (!m || !m->s.active) return fail(RIMDP_ERR_INVALID_ARGUMENT, "no active solve");
-    if (b0) *b0 = m->s.v[0].p;
-    if (b1) *b1 = m->s.v[1].p;
+    if (b0) *b0 = m->s.vb[0];
+    if (b1) *b1 = m->s.vb[1];
     return RIMDP_OK;
 }
 
@@ -1989,6 +2158,233 @@ int rimdp_model_read_columns(rimdp_model* m, int32_t cb, int32_t ce, int64_t* co
         }
         return RIMDP_OK;
     });
+}
+
+} // extern "C"
+
+// ---------------------------------------------------------------------------
+// Multi-GPU solves in one process: the model's states cut into
+// contiguous, transition-balanced shards, one per device, exchanging V over
+// peer memory every iteration (rimdp_exchange_connect_local).  The drop-in
+// layer reaches it through rimdp_b200::SolverOptions::gpus.
+
+struct rimdp_multi {
+    std::vector<rimdp_model*> shards;
+    std::vector<int> sbeg, cbeg; // state / column begin of each shard (world + 1 entries)
+    int n = 0, ncols = 0;
+    rimdp_dtype dtype = RIMDP_F64;
+    ~rimdp_multi() {
+        for (rimdp_model* m : shards) rimdp_model_destroy(m);
+    }
+};
+
+namespace {
+
+template <class T>
+int multi_solve_t(rimdp_multi* mm, const rimdp_plan* p, const rimdp_outputs* o) {
+    const int W = (int)mm->shards.size(), N = mm->n;
+    // per-shard plans: forced columns are global column indices, the shards' stores are local
+    std::vector<std::vector<int>> fl(W);
+    std::vector<rimdp_plan> pl(W, *p);
+    const long long rows = (p->forced && p->forced_time_dependent) ? std::max<long long>(p->horizon, 1) : 1;
+    if (p->forced) {
+        for (int r = 0; r < W; ++r) {
+            fl[r].assign(p->forced, p->forced + rows * N);
+            for (long long t = 0; t < rows; ++t)
+                for (int s = mm->sbeg[r]; s < mm->sbeg[r + 1]; ++s) {
+                    int& f = fl[r][t * N + s];
+                    if (f >= 0) f -= mm->cbeg[r];
+                }
+            pl[r].forced = fl[r].data();
+        }
+    }
+    for (int r = 0; r < W; ++r)
+        if (int st = check_plan(mm->shards[r], &pl[r])) return st;
+    if (p->finite ? p->horizon > 0 : true) {
+        // the first infeasible column a step evaluates: iteration rows first, then states in order
+        for (long long it = 0; it < rows; ++it)
+            for (int r = 0; r < W; ++r)
+                if (const Infeasible* f = first_evaluated_infeasible(mm->shards[r], &pl[r], it))
+                    return report_infeasible(f, mm->dtype, mm->shards[r]->col_offset);
+    }
+    for (int r = 0; r < W; ++r) {
+        rimdp_model* m = mm->shards[r];
+        DeviceGuard g(m->device);
+        upload_plan<T>(m, &pl[r]);
+        prepare_chosen(m, o, &pl[r]);
+    }
+    for (rimdp_model* m : mm->shards) { // every window reset before any rank publishes iteration 1
+        DeviceGuard g(m->device);
+        CK(cudaStreamSynchronize(m->stream));
+    }
+    auto advance_all = [&](long long it) {
+        for (rimdp_model* m : mm->shards) {
+            DeviceGuard g(m->device);
+            advance_t<T>(m, it);
+        }
+    };
+    auto poll_all = [&]() {
+        Ctl c0{};
+        for (int r = W - 1; r >= 0; --r) {
+            DeviceGuard g(mm->shards[r]->device);
+            const Ctl c = read_ctl(mm->shards[r]);
+            if (r == 0) c0 = c;
+        }
+        return c0;
+    };
+    rimdp_model* m0 = mm->shards[0];
+    const long long total = p->finite ? p->horizon : std::max<long long>(1, p->max_iterations);
+    long long k = 0;
+    Ctl c{};
+    if (o && o->on_iteration) {
+        std::vector<T> hv(N);
+        while (k < total) {
+            advance_all(1);
+            c = poll_all();
+            k = c.k;
+            DeviceGuard g(m0->device);
+            CK(cudaMemcpy(hv.data(), m0->s.vb[k & 1], sizeof(T) * N, cudaMemcpyDeviceToHost));
+            o->on_iteration(k, hv.data(), o->user);
+            if (c.done) break;
+        }
+    } else {
+        ChunkPlanner cp(p);
+        while (!c.done && m0->s.launched < total) {
+            advance_all(cp.next());
+            c = poll_all();
+            cp.observe(c.k, c.res_last);
+        }
+        k = c.k;
+    }
+    for (rimdp_model* m : mm->shards) {
+        DeviceGuard g(m->device);
+        if (read_ctl(m).status == 2) return fail(RIMDP_ERR_INTERNAL, "partial-assignment overflow in a long column");
+    }
+    {
+        DeviceGuard g(m0->device);
+        rimdp_outputs o0{};
+        if (o) {
+            o0.values = o->values;
+            o0.residual = o->residual;
+            o0.iterations = o->iterations;
+        }
+        finish_t<T>(m0, &o0, k);
+    }
+    if (o && o->chosen) {
+        const long long crow = (o->record_all_steps && p->finite) ? std::max<long long>(p->horizon, 0) : 1;
+        for (int r = 0; r < W; ++r) {
+            rimdp_model* m = mm->shards[r];
+            if (!m->s.chosen.p || m->n == 0) continue;
+            DeviceGuard g(m->device);
+            std::vector<int> loc((size_t)m->n * crow);
+            CK(cudaMemcpy(loc.data(), m->s.chosen.p, sizeof(int) * loc.size(), cudaMemcpyDeviceToHost));
+            for (long long t = 0; t < crow; ++t)
+                for (int s = 0; s < m->n; ++s) {
+                    const int ch = loc[t * m->n + s];
+                    o->chosen[t * N + mm->sbeg[r] + s] = ch >= 0 ? ch + mm->cbeg[r] : ch;
+                }
+        }
+    }
+    for (rimdp_model* m : mm->shards) m->s.active = false;
+    if (c.status == 1) {
+        fail(RIMDP_ERR_NON_CONVERGENCE, "no convergence after %lld iterations (max residual %f)", k, c.res_last);
+        g_err_info.iterations = k;
+        g_err_info.residual = c.res_last;
+        return RIMDP_ERR_NON_CONVERGENCE;
+    }
+    return RIMDP_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int rimdp_multi_create(const rimdp_model_desc* d, int32_t world, const int32_t* devices, rimdp_multi** out) {
+    if (!d || !out) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    if (world < 1 || world > kMaxWorld) return fail(RIMDP_ERR_INVALID_ARGUMENT, "world %d outside 1..%d", world, kMaxWorld);
+    if (d->num_states < 0 || d->num_cols < 0 || d->nnz < 0 || !d->stateptr || !d->colptr)
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "bad model sizes");
+    if (d->stateptr[0] != 0 || d->stateptr[d->num_states] != d->num_cols || d->colptr[0] != 0 ||
+        d->colptr[d->num_cols] != d->nnz)
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "stateptr / colptr must run from 0 to num_cols / nnz");
+    return guarded([&]() -> int {
+        std::unique_ptr<rimdp_multi> mm(new rimdp_multi);
+        mm->n = d->num_states;
+        mm->ncols = d->num_cols;
+        mm->dtype = d->dtype;
+        const int n = d->num_states;
+        const int64_t* cp = d->colptr;
+        const int32_t* sp = d->stateptr;
+        // transition-balanced cut: shard r starts at the first state whose columns begin at >= r/world of nnz
+        mm->sbeg.assign(world + 1, n);
+        mm->sbeg[0] = 0;
+        for (int r = 1; r < world; ++r) {
+            const long long target = (long long)((__int128)d->nnz * r / world);
+            int lo = mm->sbeg[r - 1], hi = n;
+            while (lo < hi) {
+                const int mid = lo + (hi - lo) / 2;
+                if (cp[sp[mid]] >= target) hi = mid;
+                else lo = mid + 1;
+            }
+            mm->sbeg[r] = lo;
+        }
+        mm->cbeg.resize(world + 1);
+        for (int r = 0; r <= world; ++r) mm->cbeg[r] = sp[mm->sbeg[r]];
+        const size_t es = elem_size(d->dtype);
+        for (int r = 0; r < world; ++r) {
+            const int sb = mm->sbeg[r], se = mm->sbeg[r + 1], cb = mm->cbeg[r], ce = mm->cbeg[r + 1];
+            const int64_t zb = cp[cb], ze = cp[ce];
+            std::vector<int32_t> lsp(se - sb + 1);
+            std::vector<int64_t> lcp(ce - cb + 1);
+            for (int s = sb; s <= se; ++s) lsp[s - sb] = sp[s] - cb;
+            for (int c = cb; c <= ce; ++c) lcp[c - cb] = cp[c] - zb;
+            rimdp_model_desc ld = *d;
+            ld.device = devices ? devices[r] : r;
+            ld.num_states = se - sb;
+            ld.num_cols = ce - cb;
+            ld.nnz = ze - zb;
+            ld.stateptr = lsp.data();
+            ld.colptr = lcp.data();
+            ld.rowval = d->rowval ? d->rowval + zb : nullptr;
+            ld.lower = d->lower ? static_cast<const char*>(d->lower) + zb * es : nullptr;
+            ld.upper = d->upper ? static_cast<const char*>(d->upper) + zb * es : nullptr;
+            rimdp_model* m = nullptr;
+            if (int st = rimdp_model_create_shard(&ld, sb, n, &m)) return st;
+            mm->shards.push_back(m);
+            m->col_offset = cb;
+            m->value_capacity = n;
+        }
+        if (int st = rimdp_exchange_connect_local(mm->shards.data(), world)) return st;
+        *out = mm.release();
+        return RIMDP_OK;
+    });
+}
+
+int rimdp_multi_solve(rimdp_multi* mm, const rimdp_plan* p, const rimdp_outputs* o) {
+    if (!mm || !p) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    if (!p->initial) return fail(RIMDP_ERR_INVALID_ARGUMENT, "plan.initial is required");
+    return guarded([&]() -> int {
+        rimdp_outputs none{};
+        return mm->dtype == RIMDP_F64 ? multi_solve_t<double>(mm, p, o ? o : &none)
+                                      : multi_solve_t<float>(mm, p, o ? o : &none);
+    });
+}
+
+int rimdp_multi_info(rimdp_multi* mm, int32_t* world, int32_t* state_begin, int32_t* devices) {
+    if (!mm) return fail(RIMDP_ERR_INVALID_ARGUMENT, "null argument");
+    const int W = (int)mm->shards.size();
+    if (world) *world = W;
+    for (int r = 0; r < W; ++r) {
+        if (state_begin) state_begin[r] = mm->sbeg[r];
+        if (devices) devices[r] = mm->shards[r]->device;
+    }
+    if (state_begin) state_begin[W] = mm->n;
+    return RIMDP_OK;
+}
+
+int rimdp_multi_destroy(rimdp_multi* mm) {
+    delete mm;
+    return RIMDP_OK;
 }
 
 } // extern "C"

@@ -2225,6 +2225,28 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
 // (the last kernel of the iteration) counts block arrivals and its last block
 // evaluates the stop test, so the residual needs no extra pass and the host
 // needs no per-iteration synchronisation.
+// Peer exchange of a state-sharded solve: every
+// shard owns an exchange window in its HBM holding the double-buffered value
+// vector, one residual slot per source rank per iteration parity and one
+// iteration flag per source rank.  The window pointers of all ranks (peer
+// device memory over NVLink: CUDA IPC or peer access) live in this table.
+constexpr int kMaxWorld = 8;
+struct PeerTable {
+    int world, rank;
+    void* v[kMaxWorld][2];                  // rank p's value buffers (V_k in buffer k & 1)
+    unsigned long long* res[kMaxWorld];     // rank p's residual slots [2][kMaxWorld] (parity, source)
+    unsigned long long* flag[kMaxWorld];    // rank p's flags [kMaxWorld]: last iteration published by each source
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 struct ActionArgs {
     int n;                         // local states
     int state_begin;               // shard offset of local state 0 in the global value vector
@@ -2242,6 +2264,7 @@ struct ActionArgs {
     int record_only;               // sharded solves: the driver owns the stop test
     int finalize;                  // this launch is the iteration's last: run the stop test
     unsigned* work;                // work counters [2 slots][kWorkKinds], slot k & 1
+    const PeerTable* peers;        // sharded solve with peer exchange, else null
 };
 
 constexpr int kWorkKinds = 4;      // 0: omax_short (q path), 1: bellman_short, 2/3: omax_medium E = 2/4
@@ -2272,7 +2295,10 @@ __device__ void iteration_epilogue(unsigned long long my, const ActionArgs& a, T
         if (m) atomicMax(&ctl->res_bits[a.k & 1], m);
         last = false;
         if (a.finalize) {
-            __threadfence();
+            // peer exchange: this block's stores into the peers' value buffers are visible system-wide
+            // before it counts as arrived
+            if (a.peers) __threadfence_system();
+            else __threadfence();
             last = atomicAdd(&ctl->arrive, 1u) == gridDim.x - 1;
         }
     }
@@ -2280,6 +2306,15 @@ __device__ void iteration_epilogue(unsigned long long my, const ActionArgs& a, T
     if (last && threadIdx.x == 0) {
         __threadfence();
         const unsigned long long rb = atomicAdd(&ctl->res_bits[a.k & 1], 0ull);
+        if (a.peers) {
+            // publish this shard's residual and iteration k to every rank (itself included); the stop test
+            // runs in peer_sync_stop once every rank has published
+            const PeerTable& pt = *a.peers;
+            for (int p = 0; p < pt.world; ++p)
+                *reinterpret_cast<volatile unsigned long long*>(pt.res[p] + (a.k & 1) * kMaxWorld + pt.rank) = rb;
+            __threadfence_system();
+            for (int p = 0; p < pt.world; ++p) st_release_sys(pt.flag[p] + pt.rank, static_cast<unsigned long long>(a.k));
+        }
         const T res = N::from_res_bits(rb);
         ctl->k = a.k;
         ctl->res_last = static_cast<double>(res);
@@ -2382,6 +2417,11 @@ action_reduce(ActionArgs a, int nstates, const int* __restrict__ states, const T
         }
         if (rewards) best = N::add(rewards[s], N::mul(discount, best));
         vout[a.state_begin + s] = best;
+        if (a.peers) { // the new value goes straight into every peer's V_k buffer (NVLink stores)
+            const PeerTable& pt = *a.peers;
+            for (int p = 0; p < pt.world; ++p)
+                if (p != pt.rank) static_cast<T*>(pt.v[p][a.k & 1])[a.state_begin + s] = best;
+        }
         if (chosen) chosen[s] = best_c;
         const unsigned long long rb = N::res_bits(fabs(N::sub(best, prev)));
         my = rb > my ? rb : my;
@@ -2637,6 +2677,48 @@ global_stop_test(int n, const T* __restrict__ vk, const T* __restrict__ vk1, Ctl
     if (finite) {
         if (k >= horizon) ctl->done = 1;
     } else if (res <= eps) {
+        ctl->done = 1;
+    } else if (k >= max_iterations) {
+        ctl->done = 1;
+        ctl->status = 1;
+    }
+    __threadfence();
+}
+
+// Stop test of iteration k of a peer-exchange sharded solve (solver.hpp:127-134).
+// One warp: lane p waits until rank p has published iteration k into this
+// shard's window (its V_k slice stores precede the flag: system-scope
+// release / acquire), then the max of the published residuals decides, so
+// every rank takes the same decision from the same numbers.  A rank that
+// already stopped returns at once (every rank stops at the same k, so no
+// flag of a later iteration is ever awaited).  Launched without PDL early
+// release, so the next iteration's kernels start only after it.
+template <class T>
+__global__ void __launch_bounds__(32)
+peer_sync_stop(Ctl* ctl, const PeerTable* __restrict__ pt, long long k, int finite, long long horizon,
+               long long max_iterations, T eps) {
+    using N = Num<T>;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    const int lane = threadIdx.x;
+    const int world = pt->world;
+    const unsigned long long* flags = pt->flag[pt->rank];
+    const unsigned long long* res = pt->res[pt->rank] + (k & 1) * kMaxWorld;
+    unsigned long long m = 0;
+    if (lane < world) {
+        while (ld_acquire_sys(flags + lane) < static_cast<unsigned long long>(k)) __nanosleep(64);
+        m = *reinterpret_cast<const volatile unsigned long long*>(res + lane);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(kFull, m, o);
+        m = x > m ? x : m;
+    }
+    if (lane != 0) return;
+    const T r = N::from_res_bits(m);
+    ctl->res_last = static_cast<double>(r);
+    if (finite) {
+        if (k >= horizon) ctl->done = 1;
+    } else if (r <= eps) {
         ctl->done = 1;
     } else if (k >= max_iterations) {
         ctl->done = 1;

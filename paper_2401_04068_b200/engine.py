@@ -108,6 +108,13 @@ _SIGNATURES = {
     "rimdp_native_read": ([C.c_char_p, _I32, _VP, _VP], C.c_int),
     "rimdp_native_take": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_native_free": ([_VP], None),
+    "rimdp_exchange_export": ([_VP, _VP], C.c_int),
+    "rimdp_exchange_connect": ([_VP, _I32, _I32, _VP], C.c_int),
+    "rimdp_exchange_connect_local": ([_VP, _I32], C.c_int),
+    "rimdp_multi_create": ([_VP, _I32, _VP, _VP], C.c_int),
+    "rimdp_multi_solve": ([_VP, _VP, _VP], C.c_int),
+    "rimdp_multi_info": ([_VP, _VP, _VP, _VP], C.c_int),
+    "rimdp_multi_destroy": ([_VP], C.c_int),
     "rimdp_random_imdp": ([_I32, _I32, _D, _D, C.c_uint64, _I32, _I32, _VP, _VP], C.c_int),
     "rimdp_random_imdp_take": ([_VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
 }
@@ -448,6 +455,101 @@ class DeviceModel:
 
     def stop_test(self):
         _check(load().rimdp_solve_stop_test(self._h))
+
+    # -- peer exchange (state-sharded solves across processes) ---------------
+    def exchange_export(self) -> bytes:
+        """This shard's exchange window as a 64-byte CUDA IPC handle (rimdp_exchange_export)."""
+        h = C.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(load().rimdp_exchange_export(self._h, h))
+        return h.raw
+
+    def exchange_connect(self, rank: int, world: int, handles: list) -> None:
+        """Map every rank's window (rank order, as exported) into this shard's peer table."""
+        blob = b"".join(handles)
+        if len(blob) != IPC_HANDLE_BYTES * world:
+            raise ValueError("one 64-byte handle per rank is required")
+        _check(load().rimdp_exchange_connect(self._h, int(rank), int(world), blob))
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def connect_local(shards) -> None:
+    """Shards of one model in this process (devices may repeat): rimdp_exchange_connect_local."""
+    arr = (C.c_void_p * len(shards))(*[m._h.value if isinstance(m._h, C.c_void_p) else m._h for m in shards])
+    _check(load().rimdp_exchange_connect_local(arr, len(shards)))
+
+
+class MultiModel:
+    """A model cut into state shards on several devices of this process, exchanging V over peer
+    memory (rimdp_multi_*).  Same solve surface as DeviceModel (global columns, whole vectors)."""
+
+    def __init__(self, stateptr, colptr, rowval, lower, upper, world: int, devices=None):
+        lower = np.asarray(lower)
+        self.dtype = np.dtype(lower.dtype)
+        sp = np.ascontiguousarray(stateptr, np.int32)
+        cp = np.ascontiguousarray(colptr, np.int64)
+        rv = np.ascontiguousarray(rowval, np.int32)
+        lo = np.ascontiguousarray(lower, self.dtype)
+        up = np.ascontiguousarray(upper, self.dtype)
+        d = ModelDesc(_dt(self.dtype), 0, len(sp) - 1, len(cp) - 1, int(cp[-1]), _p(sp), _p(cp), _p(rv), _p(lo), _p(up))
+        dev = None if devices is None else np.ascontiguousarray(devices, np.int32)
+        self._h = C.c_void_p()
+        _check(load().rimdp_multi_create(C.byref(d), int(world), _p(dev), C.byref(self._h)))
+        self.num_states = len(sp) - 1
+        self.num_cols = len(cp) - 1
+        self.nnz = int(cp[-1])
+        self.state_begin, self.state_end = 0, self.num_states
+        self.world = int(world)
+
+    def info(self):
+        w = C.c_int32()
+        sb = np.empty(self.world + 1, np.int32)
+        dv = np.empty(self.world, np.int32)
+        _check(load().rimdp_multi_info(self._h, C.byref(w), _p(sb), _p(dv)))
+        return {"world": w.value, "state_begin": sb, "devices": dv}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().rimdp_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    _plan = DeviceModel._plan
+
+    def solve(self, *, record="none", on_iteration=None, **kw):
+        plan, keep = self._plan(**kw)
+        n = self.num_states
+        values = np.empty(n, self.dtype)
+        residual = np.empty(n, self.dtype)
+        it = C.c_int64()
+        chosen = None
+        if record == "last":
+            chosen = np.empty(n, np.int32)
+        elif record == "all":
+            chosen = np.empty((max(int(kw.get("horizon", 0)), 0), n), np.int32)
+        cb = ITER_CB()
+        if on_iteration is not None:
+            dt = self.dtype
+
+            def _cb(k, vals, user):
+                arr = np.ctypeslib.as_array(C.cast(vals, C.POINTER(C.c_double if dt == np.float64 else C.c_float)),
+                                            shape=(n,)).copy()
+                on_iteration(int(k), arr)
+
+            cb = ITER_CB(_cb)
+        out = Outputs(values.ctypes.data, residual.ctypes.data, C.pointer(it), _p(chosen), int(record == "all"), cb,
+                      None)
+        _check(load().rimdp_multi_solve(self._h, C.byref(plan), C.byref(out)))
+        res = {"values": values, "residual": residual, "iterations": it.value}
+        if chosen is not None:
+            res["chosen"] = chosen
+        return res
 
     def value_buffers(self):
         b0, b1 = C.c_void_p(), C.c_void_p()

@@ -1,27 +1,33 @@
-"""State-sharded value iteration across the GPUs of one box.
+"""State-sharded value iteration across the GPUs of one box, one process per GPU.
 
-One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch for the
-plumbing).  The IMDP's states are cut into `world` contiguous ranges of equal
-length S = ceil(n / world) (state r*S .. r*S+S-1 on rank r): every rank holds
-the columns of its own states in HBM and a full replica of the value vector,
-padded to world * S entries.  Per iteration k each rank
+The IMDP's states are cut into `world` contiguous ranges (``shard_ranges``);
+every rank holds the columns of its own states in HBM and a full replica of
+the value vector.  Per iteration k each rank runs the Bellman kernels for its
+states, and the exchange is fused into them:
 
-  1. runs the Bellman kernels for its states (writes V_k[r*S : r*S+S]),
-  2. all-gathers the slices in place into its replica of V_k (one
-     ncclAllGather of S entries per rank — the only collective),
-  3. enqueues the device stop test (solver.hpp:127-134): every rank now holds
-     V_k and V_{k-1} in full, so the global residual max |V_k - V_{k-1}| is
-     reduced on the device over the whole vector, with no second collective,
+  * the action kernel stores every new value V_k[s] of the rank's states into
+    every peer's V_k buffer over NVLink (peer memory mapped with CUDA IPC) as
+    it computes it — the transfer overlaps the computation of the local rows
+    by construction, there is no separate collective;
+  * its last block publishes the rank's residual and the iteration number to
+    every peer (system-scope release);
+  * a one-warp kernel (peer_sync_stop) waits for every rank's flag of
+    iteration k (acquire) and runs the stop test (solver.hpp:127-134) on the
+    maximum published residual — the same numbers, so the same decision, on
+    every rank.
 
-all on the shard's CUDA stream, so iterations are enqueued ahead without host
-synchronisation; the host polls once per chunk.  Kernels after the stop
-iteration are no-ops and the collectives after it re-exchange unchanged
-slices, so the result is the stopping iterate on every rank.  Per-state
+All of it is stream-ordered on the shard's CUDA stream, so iterations are
+enqueued ahead without host synchronisation; the host polls once per chunk.
+Kernels after the stop iteration are no-ops on every rank.  Per-state
 arithmetic is unchanged by sharding: results are bit-identical to one GPU.
 
-The equal-length cut keeps the exchange a single in-place all-gather; for the
-synthetic laws of configs 2-5 it is also nnz-balanced to within a few percent
-(reported by ``shard_balance``).  See DESIGN.md "Multi-GPU".
+``torch.distributed`` is plumbing only: the 64-byte IPC handles of the
+exchange windows are swapped once with ``all_gather_object`` and every
+solve's begin is followed by one barrier (begin resets the windows).
+
+``NcclShard`` keeps the unfused baseline for comparison: local kernels, then
+an in-place ``all_gather`` of the padded V slices with NCCL, then a device
+stop test over the gathered vector — three steps per iteration on one stream.
 """
 from __future__ import annotations
 
@@ -32,7 +38,7 @@ import numpy as np
 
 
 def shard_ranges(n: int, world: int) -> list[tuple[int, int]]:
-    """[(state_begin, state_end)] per rank: equal-length contiguous cuts (last may be short or empty)."""
+    """[(state_begin, state_end)] per rank: equal-length contiguous cuts (the last may be short or empty)."""
     if n < 0 or world < 1:
         raise ValueError("bad sizes")
     S = max(1, math.ceil(n / world))
@@ -61,6 +67,36 @@ def slice_csc(stateptr, colptr, rowval, lower, upper, sb: int, se: int):
     return (stateptr[sb:se + 1] - cb, colptr[cb:ce + 1] - b, rowval[b:e], lower[b:e], upper[b:e])
 
 
+class PeerShard:
+    """The engine's shard (a DeviceModel built for states [sb, se)) connected to its peers' exchange
+    windows: one collective at construction (the IPC handles), none per iteration."""
+
+    fused = True
+
+    def __init__(self, model, rank: int, world: int, n_global: int, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.model = model
+        self.rank, self.world, self.n = rank, world, n_global
+        model.set_value_capacity(n_global)
+        handles = [None] * world
+        dist.all_gather_object(handles, model.exchange_export(), group=group)
+        model.exchange_connect(rank, world, handles)
+
+    def begin(self, **plan):
+        self.model.begin(**plan, external_stop=True)
+        self.dist.barrier(group=self.group)  # every window is reset before any rank publishes iteration 1
+
+    def advance(self, iterations: int):
+        self.model.advance(iterations)       # kernels + peer stores + peer_sync_stop, per iteration
+
+    def poll(self):
+        return self.model.poll()
+
+    def finish(self):
+        return self.model.finish()
+
+
 class _CudaArray:
     """__cuda_array_interface__ view of a raw device pointer (for torch.as_tensor)."""
 
@@ -69,15 +105,21 @@ class _CudaArray:
                                          "strides": None}
 
 
-class DeviceShard:
-    """The engine's shard (a DeviceModel built for states [sb, se)) as seen by the driver."""
+class NcclShard:
+    """Unfused baseline: V padded to world equal slices, one in-place NCCL all-gather and a device stop test
+    over the gathered vector after each iteration's kernels."""
 
-    def __init__(self, model, rank: int, world: int, n_global: int):
+    fused = False
+
+    def __init__(self, model, rank: int, world: int, n_global: int, group=None):
         import torch
-        self.torch = torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
         self.model = model
         self.rank, self.world, self.n = rank, world, n_global
         self.S = slice_length(n_global, world)
+        if shard_ranges(n_global, world)[rank][0] != min(n_global, rank * self.S):
+            raise ValueError("the NCCL baseline needs equal-length slices (shard_ranges)")
         self.capacity = self.S * world
         model.set_value_capacity(self.capacity)
         self.device = torch.device("cuda", model.info().device)
@@ -85,26 +127,26 @@ class DeviceShard:
 
     def begin(self, **plan):
         self.model.begin(**plan, external_stop=True)
-        t = self.torch
         ts = "<f8" if self.model.dtype == np.float64 else "<f4"
         b0, b1 = self.model.value_buffers()
-        self.values = [t.as_tensor(_CudaArray(b, self.capacity, ts), device=self.device) for b in (b0, b1)]
-        self.residual = t.as_tensor(_CudaArray(self.model.residual_slots(), 2, "<i8"), device=self.device)
+        self.values = [self.torch.as_tensor(_CudaArray(b, self.capacity, ts), device=self.device) for b in (b0, b1)]
+        self.k = 0
 
-    def advance(self):
-        self.model.advance(1)
-
-    def stop_test(self):
-        self.model.stop_test()
+    def advance(self, iterations: int):
+        with self.torch.cuda.stream(self.stream):
+            for _ in range(iterations):
+                self.k += 1
+                self.model.advance(1)
+                buf = self.values[self.k & 1]
+                r, S = self.rank, self.S
+                self.dist.all_gather_into_tensor(buf, buf[r * S:(r + 1) * S], group=self.group)
+                self.model.stop_test()
 
     def poll(self):
         return self.model.poll()
 
     def finish(self):
         return self.model.finish()
-
-    def stream_context(self):
-        return self.torch.cuda.stream(self.stream)
 
 
 @dataclass
@@ -125,45 +167,37 @@ class NonConvergence(RuntimeError):
 
 
 class ShardedSolver:
-    """Drives one rank's shard through a sharded solve (the loop of
-    detail::iterate, solver.hpp:85-137, with the exchange step added)."""
+    """Drives one rank's shard through a sharded solve (the loop of detail::iterate, solver.hpp:85-137,
+    with the exchange fused into the iteration)."""
 
-    def __init__(self, shard, group=None, chunk: int = 32):
-        import torch.distributed as dist
-        self.dist = dist
+    def __init__(self, shard, group=None, chunk: int = 64):
         self.shard = shard
         self.group = group
         self.chunk = chunk
 
-    def _exchange(self, k: int):
-        sh, dist = self.shard, self.dist
-        buf = sh.values[k & 1]
-        r, S = sh.rank, sh.S
-        dist.all_gather_into_tensor(buf, buf[r * S:(r + 1) * S], group=self.group)
-
-    def enqueue(self, k: int):
-        """Iteration k: local kernels, exchange, stop test — all stream-ordered."""
-        self.shard.advance()
-        self._exchange(k)
-        self.shard.stop_test()
-
     def solve(self, *, finite: bool, horizon: int = 0, max_iterations: int = 1_000_000, eps: float = 0.0,
               **plan) -> ShardedResult:
         sh = self.shard
-        total = horizon if finite else max_iterations
+        total = horizon if finite else max(1, max_iterations)  # iterate() always runs step 1
         sh.begin(finite=finite, horizon=horizon, max_iterations=max_iterations, eps=eps, **plan)
-        k = 0
-        done = False
-        res = 0.0
-        with sh.stream_context():
-            while k < total and not done:
-                for _ in range(min(self.chunk, total - k)):
-                    k += 1
-                    self.enqueue(k)
-                _, done, res = sh.poll()
+        launched, done, res = 0, False, 0.0
+        step, last = 4, None
+        while launched < total and not done:
+            n = min(step, total - launched)
+            sh.advance(n)
+            launched += n
+            k, done, res = sh.poll()
+            # geometric residual decay near convergence: enqueue about as many as the stop test needs
+            if not finite and last and 0 < res < last[1] and k > last[0] and eps > 0:
+                rate = math.log(res / last[1]) / (k - last[0])
+                need = math.log(eps / res) / rate
+                step = max(1, min(int(need) + 1, self.chunk)) if math.isfinite(need) else min(2 * step, self.chunk)
+            else:
+                step = min(2 * step, self.chunk)
+            last = (k, res)
         out = sh.finish()
         iters = out["iterations"]
-        if not finite and iters > 0 and not res <= np.dtype(sh.model.dtype).type(eps):
+        dt = getattr(getattr(sh, "model", None), "dtype", np.float64)
+        if not finite and not res <= np.dtype(dt).type(eps):
             raise NonConvergence(iters, res)
         return ShardedResult(out["values"][:sh.n], out["residual"][:sh.n], iters, True)
-

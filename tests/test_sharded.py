@@ -4,10 +4,8 @@ its states' rows with the CPU checker (oracle port).  Covers the partitioning,
 the padded in-place all-gather of V, the external stop test on the
 residual of the gathered iterates and NonConvergence — and that the sharded result is
 bit-identical to the unsharded one (per-state arithmetic is unchanged)."""
-import contextlib
 import os
 import socket
-import struct
 
 import numpy as np
 import pytest
@@ -46,15 +44,18 @@ def test_shard_balance_of_synthetic_laws():
 
 
 class CpuShard:
-    """Test double of sharded.DeviceShard: same protocol, CPU tensors, rows
-    of states [sb, se) computed by the oracle port's Bellman step."""
+    """Test double of sharded.PeerShard: the same protocol (begin + barrier, advance(n), poll, finish) on
+    the CPU.  The rows of states [sb, se) come from the oracle port's Bellman step; the exchange the engine
+    fuses into its action kernel (peer stores of the new slice + a published residual per rank) is staged
+    through the host with one all_gather_object per iteration, and the stop test takes the max of the
+    published residuals, as peer_sync_stop does."""
 
-    def __init__(self, arrays, rank, world):
+    fused = True
+
+    def __init__(self, arrays, rank, world, group=None):
         self.cpu = oracle.Model.from_arrays("port", *arrays)
         self.n = len(arrays[0]) - 1
-        self.rank, self.world = rank, world
-        self.S = sharded.slice_length(self.n, world)
-        self.capacity = self.S * world
+        self.rank, self.world, self.group = rank, world, group
         self.sb, self.se = sharded.shard_ranges(self.n, world)[rank]
 
         class M:
@@ -63,59 +64,46 @@ class CpuShard:
 
     def begin(self, *, initial, frozen=None, rewards=None, discount=0.0, pessimistic=True, maximize=True,
               finite=True, horizon=0, eps=0.0, max_iterations=1_000_000, external_stop=True):
-        self.values = [torch.zeros(self.capacity, dtype=torch.float64) for _ in range(2)]
-        for b in self.values:
-            b[:self.n] = torch.from_numpy(np.asarray(initial, np.float64))
-        self.residual = torch.zeros(2, dtype=torch.int64)
+        self.values = [np.asarray(initial, np.float64).copy() for _ in range(2)]
         self.plan = dict(frozen=frozen, rewards=rewards, discount=discount, pess=pessimistic, maxi=maximize,
-                         finite=finite, horizon=horizon, eps=eps, max_iterations=max_iterations)
-        self.launched = self.k = 0
+                         finite=finite, horizon=horizon, eps=eps, max_iterations=max(1, max_iterations))
+        self.k = 0
         self.done = False
         self.res_last = 0.0
+        dist.barrier(group=self.group)
 
-    def advance(self):
-        k = self.launched = self.launched + 1
-        if self.done:
-            return
-        p = self.plan
-        prev = self.values[(k - 1) & 1][:self.n].numpy().copy()
-        v, _ = self.cpu.bellman_step(prev, p["pess"], p["maxi"], p["frozen"])
-        if p["rewards"] is not None:
-            v = p["rewards"] + p["discount"] * v
-        out = self.values[k & 1]
-        out[self.sb:self.se] = torch.from_numpy(v[self.sb:self.se])
-        res = float(np.max(np.abs(v[self.sb:self.se] - prev[self.sb:self.se]), initial=0.0))
-        self.residual[k & 1] = struct.unpack("<q", struct.pack("<d", res))[0]
-        self.residual[(k + 1) & 1] = 0
-        self.k = k
-
-    def stop_test(self):
-        # like the device kernel: the residual over the whole gathered vector
-        if self.done:
-            return
-        k, p = self.k, self.plan
-        full = float(torch.max(torch.abs(self.values[k & 1][:self.n] - self.values[(k - 1) & 1][:self.n])))
-        local = struct.unpack("<d", struct.pack("<q", int(self.residual[k & 1])))[0]
-        res = max(full, local)
-        self.res_last = res
-        if p["finite"]:
-            self.done = k >= p["horizon"]
-        elif res <= p["eps"]:
-            self.done = True
-        elif k >= p["max_iterations"]:
-            self.done = True
+    def advance(self, iterations):
+        for _ in range(iterations):
+            if self.done:
+                return
+            k = self.k + 1
+            p = self.plan
+            prev = self.values[(k - 1) & 1]
+            v, _ = self.cpu.bellman_step(prev, p["pess"], p["maxi"], p["frozen"])
+            if p["rewards"] is not None:
+                v = p["rewards"] + p["discount"] * v
+            mine = v[self.sb:self.se]
+            res = float(np.max(np.abs(mine - prev[self.sb:self.se]), initial=0.0))
+            got = [None] * self.world
+            dist.all_gather_object(got, (self.sb, mine, res), group=self.group)  # the "peer stores"
+            out = self.values[k & 1]
+            for sb, sl, _ in got:
+                out[sb:sb + len(sl)] = sl
+            r = max(x[2] for x in got)
+            self.k, self.res_last = k, r
+            if p["finite"]:
+                self.done = k >= p["horizon"]
+            elif r <= p["eps"] or k >= p["max_iterations"]:
+                self.done = True
 
     def poll(self):
         return self.k, self.done, self.res_last
 
     def finish(self):
         k = self.k
-        v = self.values[k & 1][:self.n].numpy().copy()
-        r = np.abs(v - self.values[(k - 1) & 1][:self.n].numpy()) if k else np.zeros(self.n)
+        v = self.values[k & 1].copy()
+        r = np.abs(v - self.values[(k - 1) & 1]) if k else np.zeros(self.n)
         return {"values": v, "residual": r, "iterations": k}
-
-    def stream_context(self):
-        return contextlib.nullcontext()
 
 
 def _free_port():
@@ -130,7 +118,7 @@ def _worker(rank, world, port, arrays, cases, q):
     try:
         out = []
         for plan in cases:
-            solver = sharded.ShardedSolver(CpuShard(arrays, rank, world), chunk=5)
+            solver = sharded.ShardedSolver(CpuShard(arrays, rank, world), chunk=5)  # 5: chunks end mid-solve
             try:
                 r = solver.solve(**plan)
                 out.append((r.values, r.iterations))
@@ -154,11 +142,11 @@ def _cases(n):
     ]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_solve_bit_identical_to_unsharded(world):
+@pytest.mark.parametrize("world,n", [(2, 37), (3, 37), (4, 9)])
+def test_sharded_solve_bit_identical_to_unsharded(world, n):
+    """37 states: unequal slices; 9 states over 4 ranks: the last rank owns no state."""
     oracle.build(ref=False)
-    arrays = engine.random_imdp(37, 3, 0.25, 0.2, 12)  # 37 states: the last slice is padded
-    n = 37
+    arrays = engine.random_imdp(n, 3, 0.25 if n > 20 else 0.5, 0.2, 12)
     cases = _cases(n)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -170,6 +158,8 @@ def test_sharded_solve_bit_identical_to_unsharded(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    if n == 9:
+        assert sharded.shard_ranges(n, world)[-1][0] == sharded.shard_ranges(n, world)[-1][1]
     # unsharded reference: the same loop in one process (world 1)
     cpu = oracle.Model.from_arrays("port", *arrays)
     for i, plan in enumerate(cases):
