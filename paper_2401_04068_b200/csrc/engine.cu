@@ -1327,6 +1327,9 @@ int report_infeasible(const Infeasible* f, rimdp_dtype dtype, int col_offset = 0
 template <class T>
 int solve_begin_t(rimdp_model* m, const rimdp_plan* p) {
     upload_plan<T>(m, p);
+    // a connected shard's window (V_0 in both buffers, zeroed flags) must be in place before the driver's
+    // barrier lets any peer store iteration 1 into it
+    if (m->x.connected) CK(cudaStreamSynchronize(m->stream));
     return RIMDP_OK;
 }
 
@@ -2217,11 +2220,15 @@ int multi_solve_t(rimdp_multi* mm, const rimdp_plan* p, const rimdp_outputs* o) 
         DeviceGuard g(m->device);
         CK(cudaStreamSynchronize(m->stream));
     }
+    // one iteration per shard in turn: a launch that blocks on a full launch queue (a shard's kernels wait in
+    // peer_sync_stop for the other shards' flags) then always finds the other shards' same iteration
+    // already enqueued, so they can progress and drain it
     auto advance_all = [&](long long it) {
-        for (rimdp_model* m : mm->shards) {
-            DeviceGuard g(m->device);
-            advance_t<T>(m, it);
-        }
+        for (long long i = 0; i < it; ++i)
+            for (rimdp_model* m : mm->shards) {
+                DeviceGuard g(m->device);
+                advance_t<T>(m, 1);
+            }
     };
     auto poll_all = [&]() {
         Ctl c0{};

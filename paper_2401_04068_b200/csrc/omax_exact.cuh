@@ -92,8 +92,10 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
     using Sh = ExactShape<LG>;
     constexpr int N = Sh::N, NT = Sh::NT, E = Sh::E;
     pdl_enter();
+    // the other launch parity's fallback count is cleared even by a no-op launch after the stop: the host
+    // flips the parity for every launch
+    if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) *fb_other = 0;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) *fb_other = 0; // the other launch parity's count
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned* cnt = reinterpret_cast<unsigned*>(smem_raw);                                       // N + 1
     unsigned long long* tmp = reinterpret_cast<unsigned long long*>(smem_raw + ((N + 1) * 4 + 15) / 16 * 16);

@@ -470,6 +470,11 @@ class DeviceModel:
             raise ValueError("one 64-byte handle per rank is required")
         _check(load().rimdp_exchange_connect(self._h, int(rank), int(world), blob))
 
+    def value_buffers(self):
+        b0, b1 = C.c_void_p(), C.c_void_p()
+        _check(load().rimdp_solve_value_buffers(self._h, C.byref(b0), C.byref(b1)))
+        return b0.value, b1.value
+
 
 IPC_HANDLE_BYTES = 64
 
@@ -550,8 +555,3 @@ class MultiModel:
         if chosen is not None:
             res["chosen"] = chosen
         return res
-
-    def value_buffers(self):
-        b0, b1 = C.c_void_p(), C.c_void_p()
-        _check(load().rimdp_solve_value_buffers(self._h, C.byref(b0), C.byref(b1)))
-        return b0.value, b1.value
