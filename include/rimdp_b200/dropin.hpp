@@ -35,6 +35,7 @@
 #include "rimdp/numeric.hpp"
 #include "rimdp/omax.hpp"
 #include "rimdp/property.hpp"
+#include "rimdp/solver.hpp"
 
 #include <charconv>
 #include <cstdint>
@@ -48,6 +49,32 @@
 namespace rimdp_b200 {
 
 using rimdp::index_t;
+
+/// rimdp::SolverOptions (solver.hpp:19-23) plus the engine's placement fields
+/// ("a GPU-count option is added as a new field").  Any options
+/// type works with the entry points below; these fields are read when present.
+struct SolverOptions : rimdp::SolverOptions {
+    int device = 0;            ///< single-GPU solves
+    int gpus = 1;              ///< > 1: state-sharded over devices 0 .. gpus-1, V exchanged over NVLink
+    std::vector<int> devices;  ///< explicit shard devices (may repeat); overrides gpus when non-empty
+};
+
+/// Where an Engine puts the model: one device, or one shard per entry of `devices`.
+struct Placement {
+    int device = 0;
+    std::vector<int> devices;  ///< empty or one entry: single device
+};
+
+template <typename Options>
+Placement placement_of(const Options& o) {
+    Placement p;
+    if constexpr (requires { o.device; }) p.device = o.device;
+    if constexpr (requires { o.devices; }) p.devices.assign(o.devices.begin(), o.devices.end());
+    if constexpr (requires { o.gpus; })
+        if (p.devices.empty() && o.gpus > 1)
+            for (int g = 0; g < o.gpus; ++g) p.devices.push_back(g);
+    return p;
+}
 
 template <typename Value>
 inline constexpr bool has_device_path = std::is_same_v<Value, double> || std::is_same_v<Value, float>;
@@ -196,14 +223,18 @@ rimdp::IntervalMDP<Value> read_native_model(const std::string& path) {
 template <typename Value>
 class Engine {
 public:
-    explicit Engine(const rimdp::IntervalMDP<Value>& mdp, int device = 0) : mdp_(&mdp) {
+    explicit Engine(const rimdp::IntervalMDP<Value>& mdp, int device = 0) : Engine(mdp, Placement{device, {}}) {}
+
+    /// Placement with several devices: the model cut into transition-balanced state shards, one per
+    /// device, solved together (rimdp_multi_*); results are bit-identical to one device.
+    Engine(const rimdp::IntervalMDP<Value>& mdp, const Placement& where) : mdp_(&mdp) {
         const auto& tp = mdp.transition();
         const auto cp32 = tp.colptr();
         std::vector<std::int64_t> colptr(cp32.begin(), cp32.end()); // int64 on the device
         if (colptr.empty()) colptr.push_back(0);
         rimdp_model_desc d{};
         d.dtype = dtype_of<Value>();
-        d.device = device;
+        d.device = where.device;
         d.num_states = mdp.num_states();
         d.num_cols = mdp.num_cols();
         d.nnz = tp.nnz();
@@ -212,13 +243,25 @@ public:
         d.rowval = tp.rowval().data();
         d.lower = tp.lower_values().data();
         d.upper = tp.upper_values().data();
-        detail::check(rimdp_model_create(&d, &model_), d.dtype);
+        d.device = where.device;
+        if (where.devices.size() > 1) {
+            detail::check(rimdp_multi_create(&d, static_cast<int32_t>(where.devices.size()), where.devices.data(),
+                                             &multi_),
+                          d.dtype);
+        } else {
+            if (where.devices.size() == 1) d.device = where.devices[0];
+            detail::check(rimdp_model_create(&d, &model_), d.dtype);
+        }
     }
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
-    ~Engine() { rimdp_model_destroy(model_); }
+    ~Engine() {
+        rimdp_model_destroy(model_);
+        rimdp_multi_destroy(multi_);
+    }
 
     rimdp_model* handle() const { return model_; }
+    bool sharded() const { return multi_ != nullptr; }
     const rimdp::IntervalMDP<Value>& mdp() const { return *mdp_; }
 
     template <typename Options>
@@ -296,6 +339,7 @@ public:
 
     rimdp::BellmanResult<Value> bellman_step(std::span<const Value> v_prev, rimdp::OptimizationMode mode,
                                              std::span<const std::uint8_t> frozen = {}) {
+        if (multi_) throw rimdp::Error("rimdp_b200: bellman_step runs on a single-device Engine");
         const index_t n = mdp_->num_states();
         if (static_cast<index_t>(v_prev.size()) != n)
             throw rimdp::Error("rimdp_b200: value vector has " + std::to_string(v_prev.size()) + " entries for " +
@@ -314,6 +358,7 @@ public:
 
     /// Robust expectation of every column (bellman.hpp:60-70 for all columns at once).
     std::vector<Value> column_values(std::span<const Value> values, rimdp::SatisfactionMode mode) {
+        if (multi_) throw rimdp::Error("rimdp_b200: column_values runs on a single-device Engine");
         std::vector<Value> q(static_cast<std::size_t>(mdp_->num_cols()));
         detail::check(rimdp_column_values(model_, values.data(), mode == rimdp::SatisfactionMode::Pessimistic,
                                           q.data()),
@@ -365,36 +410,40 @@ private:
             };
             o.user = &cb;
         }
-        detail::check(rimdp_solve(model_, &p, &o), dtype_of<Value>());
+        detail::check(multi_ ? rimdp_multi_solve(multi_, &p, &o) : rimdp_solve(model_, &p, &o), dtype_of<Value>());
         vf.iterations = iters;
         return vf;
     }
 
     const rimdp::IntervalMDP<Value>* mdp_;
     rimdp_model* model_ = nullptr;
+    rimdp_multi* multi_ = nullptr;
 };
 
 // ---- free functions with the reference's signatures ------------------------
 
-template <typename Value, typename Options>
-rimdp::ValueFunction<Value> value_iteration(const rimdp::Problem<Value>& problem, const Options& options) {
-    Engine<Value> e(problem.imdp);
+// Options defaults to rimdp_b200::SolverOptions (a rimdp::SolverOptions), so
+// `value_iteration(problem)` works as in the reference (solver.hpp:149-155).
+
+template <typename Value, typename Options = SolverOptions>
+rimdp::ValueFunction<Value> value_iteration(const rimdp::Problem<Value>& problem, const Options& options = {}) {
+    Engine<Value> e(problem.imdp, placement_of(options));
     return e.value_iteration(problem.spec, options);
 }
 
-template <typename Value, typename Options>
+template <typename Value, typename Options = SolverOptions>
 std::pair<rimdp::Policy, rimdp::ValueFunction<Value>> control_synthesis(const rimdp::Problem<Value>& problem,
-                                                                        const Options& options) {
-    Engine<Value> e(problem.imdp);
+                                                                        const Options& options = {}) {
+    Engine<Value> e(problem.imdp, placement_of(options));
     return e.control_synthesis(problem.spec, options);
 }
 
-template <typename Value, typename Options>
+template <typename Value, typename Options = SolverOptions>
 rimdp::ValueFunction<Value> verify_policy(const rimdp::IntervalMDP<Value>& mdp, const rimdp::Policy& policy,
-                                          const rimdp::Specification<Value>& spec, const Options& options) {
+                                          const rimdp::Specification<Value>& spec, const Options& options = {}) {
     // the reference validates the property before touching the model (solver.hpp:208)
     (void)detail::make_plan(spec, mdp.num_states());
-    Engine<Value> e(mdp);
+    Engine<Value> e(mdp, placement_of(options));
     return e.verify_policy(policy, spec, options);
 }
 

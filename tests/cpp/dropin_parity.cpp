@@ -107,6 +107,21 @@ void compare_solve(const std::string& name, const Problem<Value>& pr, double tol
     auto vi = rimdp_b200::value_iteration(pr, o);
     EXPECT(same(vi.values, gv.values, 0), "%s value_iteration == control_synthesis", name.c_str());
     EXPECT(vi.iterations == gv.iterations, "%s iterations vi/cs", name.c_str());
+    if (max_iter == 1'000'000) { // the reference's default options (solver.hpp:149-155)
+        auto vd = rimdp_b200::value_iteration(pr);
+        EXPECT(same(vd.values, gv.values, 0) && vd.iterations == gv.iterations, "%s default options", name.c_str());
+    }
+    // the sharded multi-GPU solve (SolverOptions::devices; two and three shards on device 0 here): the
+    // same bits as one device, strategies included
+    for (int world : {2, 3}) {
+        rimdp_b200::SolverOptions mo;
+        mo.max_iterations = max_iter;
+        mo.devices.assign(world, 0);
+        auto [mp, mv] = rimdp_b200::control_synthesis(pr, mo);
+        EXPECT(mv.iterations == gv.iterations && same(mv.values, gv.values, 0) && same(mv.residual, gv.residual, 0) &&
+                   same_policy(mp, gp),
+               "%s sharded x%d == single device", name.c_str(), world);
+    }
     // re-verify the synthesized policy (solver.hpp:204-251)
     auto rver = rimdp::verify_policy(pr.imdp, rp, pr.spec, o);
     auto gver = rimdp_b200::verify_policy(pr.imdp, rp, pr.spec, o);
