@@ -42,7 +42,7 @@ def test_library_is_sm100a():
 
 
 def test_abi_version_and_error_path_without_device(engine_lib):
-    assert engine_lib.rimdp_abi_version() == 3
+    assert engine_lib.rimdp_abi_version() == 4
     if engine.device_count() > 0:
         pytest.skip("a device is visible")
     with pytest.raises(engine.EngineError) as ei:
