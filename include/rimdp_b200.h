@@ -45,7 +45,9 @@ typedef enum rimdp_status {
     RIMDP_ERR_NO_DEVICE = 6,
     RIMDP_ERR_INTERNAL = 7,
     RIMDP_ERR_MISSING_FILE = 8,      /* io::MissingFile (errors.hpp), native model containers */
-    RIMDP_ERR_SCHEMA = 9             /* io::SchemaViolation (errors.hpp:92-95), native.hpp:459-461 */
+    RIMDP_ERR_SCHEMA = 9,            /* io::SchemaViolation (errors.hpp:92-95), native.hpp:459-461 */
+    RIMDP_ERR_INVALID_MODEL = 10     /* ModelError from the upload checks: StructuralError (csc.hpp:89-104),
+                                        EntryOutOfRange / BoundOrderViolation (interval.hpp:148-164) */
 } rimdp_status;
 
 typedef struct rimdp_model rimdp_model; /* opaque, owns the device CSC store */
@@ -58,6 +60,8 @@ typedef struct rimdp_error_info {
     int64_t column;          /* INFEASIBLE_COLUMN: offending column */
     int32_t infeasible_kind; /* 1: lower bounds sum > 1 + tol, 2: upper bounds sum < 1 - tol */
     double infeasible_sum;   /* the sum quoted by the reference message */
+    int32_t violation_kind;  /* INVALID_MODEL: rimdp::ViolationKind value (errors.hpp:18-27) */
+    int64_t row;             /* INVALID_MODEL: destination row of the offending entry */
 } rimdp_error_info;
 
 const char* rimdp_last_error(void);
@@ -86,6 +90,14 @@ typedef struct rimdp_model_desc {
     const void* upper;       /* [nnz] dtype */
 } rimdp_model_desc;
 
+/* Checks at upload, on the device, in the reference's report order
+ * (IntervalProbabilities::validate, interval.hpp:132-179, first violation as
+ * check_or_throw :254-258): rows in range and strictly increasing per column,
+ * bounds finite in [0,1], lower <= upper -> RIMDP_ERR_INVALID_MODEL with the
+ * reference's ModelError text and the kind / column / row in
+ * rimdp_error_info.  Column sums are not rejected here: an infeasible column
+ * is reported when a step evaluates it (RIMDP_ERR_INFEASIBLE_COLUMN), as the
+ * reference's step does for unchecked models (omax.hpp:72-80). */
 int rimdp_model_create(const rimdp_model_desc* desc, rimdp_model** out);
 /* One shard of a model for state-sharded multi-GPU solves: `desc` holds the
  * local states [state_begin, state_begin + desc->num_states) only (stateptr

@@ -112,6 +112,13 @@ template <typename Value>
     }
     case RIMDP_ERR_NON_CONVERGENCE:
         throw rimdp::NonConvergence(info.iterations, info.residual);
+    case RIMDP_ERR_INVALID_MODEL: {
+        // the upload checks (interval.hpp:132-179): the message is Violation::to_string, "<Kind> ...: <text>"
+        const auto colon = msg.find(": ");
+        rimdp::Violation v{static_cast<rimdp::ViolationKind>(info.violation_kind),
+                           colon == std::string::npos ? msg : msg.substr(colon + 2), info.column, info.row};
+        throw rimdp::ModelError(std::move(v));
+    }
     default:
         throw rimdp::Error("rimdp_b200: " + msg);
     }

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <charconv>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -36,6 +37,7 @@ namespace {
 
 thread_local std::string g_err_msg;
 thread_local rimdp_error_info g_err_info{};
+thread_local int g_shard_col_offset = 0; // rimdp_multi_create: global index of the shard being created's column 0
 
 struct Fail {
     int status;
@@ -616,6 +618,54 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     CK(cudaStreamSynchronize(m->stream));
 }
 
+// Reference text of a float (NumericTraits::to_string, numeric.hpp:30-35: std::to_chars shortest form).
+template <class T>
+std::string num_text(T v) {
+    char buf[64];
+    const auto r = std::to_chars(buf, buf + sizeof buf, v);
+    return std::string(buf, r.ptr);
+}
+
+// The first violation validate_entries found, as the reference's ModelError (errors.hpp:44-55,
+// Violation::to_string :155-162): "<Kind> column=<j> row=<r>: <message>".
+template <class T>
+void report_violation(rimdp_model* m, const unsigned long long* hf) {
+    const bool structural = hf[0] != ~0ull;
+    const unsigned long long key = structural ? hf[0] : hf[1];
+    const int col = (int)(key >> 32);
+    const unsigned low = (unsigned)key;
+    const long long k = structural ? (low >> 1) : (low >> 2);
+    long long b = 0;
+    CK(cudaMemcpy(&b, m->colptr.as<long long>() + col, sizeof b, cudaMemcpyDeviceToHost));
+    int row = 0;
+    T l{}, u{};
+    CK(cudaMemcpy(&row, m->rows.as<int>() + b + k, sizeof row, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&l, m->lower.as<T>() + b + k, sizeof l, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&u, m->gap.as<T>() + b + k, sizeof u, cudaMemcpyDeviceToHost)); // still the upper bounds here
+    std::string kind, msg;
+    int vk;
+    if (structural) {
+        kind = "StructuralError";
+        vk = 7;
+        msg = (low & 1) ? "row indices not strictly increasing within column" : "row index out of range";
+    } else if ((low & 3) == 2) {
+        kind = "BoundOrderViolation";
+        vk = 2;
+        msg = "lower bound " + num_text(l) + " exceeds upper bound " + num_text(u);
+    } else {
+        kind = "EntryOutOfRange";
+        vk = 1;
+        msg = std::string((low & 3) == 0 ? "lower" : "upper") + " bound " + num_text((low & 3) == 0 ? l : u) +
+              " outside [0,1]";
+    }
+    // Violation::to_string prints row= only for row >= 0 (errors.hpp:155-162)
+    const std::string where = row >= 0 ? " row=" + std::to_string(row) : std::string();
+    fail(RIMDP_ERR_INVALID_MODEL, "%s column=%d%s: %s", kind.c_str(), col + m->col_offset, where.c_str(), msg.c_str());
+    g_err_info.column = col + m->col_offset;
+    g_err_info.row = row;
+    g_err_info.violation_kind = vk;
+}
+
 template <class T>
 void prepare(rimdp_model* m) {
     m->rem.ensure(sizeof(T) * std::max(1, m->ncols));
@@ -625,9 +675,19 @@ void prepare(rimdp_model* m) {
     m->scratch.ensure(64);
     CK(cudaMemsetAsync(m->scratch.p, 0, 64, m->stream));
     int* counters = m->scratch.as<int>();
-    if (m->nnz > 0)
-        check_rows<<<grid_for(m->nnz, 256, m->sm_count, 8), 256, 0, m->stream>>>(m->nnz, m->rows.as<int>(), m->n_global,
-                                                                              counters + 1);
+    unsigned long long* first = reinterpret_cast<unsigned long long*>(m->scratch.as<char>() + 16);
+    const unsigned long long none[2] = {~0ull, ~0ull};
+    CK(cudaMemcpyAsync(first, none, sizeof none, cudaMemcpyHostToDevice, m->stream));
+    if (m->ncols > 0)
+        validate_entries<T><<<grid_for(m->ncols, 8, m->sm_count, 8), 256, 0, m->stream>>>(
+            m->ncols, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->n_global, first);
+    unsigned long long hf[2];
+    CK(cudaMemcpyAsync(hf, first, sizeof hf, cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    if (hf[0] != ~0ull || hf[1] != ~0ull) {
+        report_violation<T>(m, hf);
+        throw Fail{RIMDP_ERR_INVALID_MODEL};
+    }
     if (m->ncols > 0)
         prepare_columns<T><<<grid_for(m->ncols, 8, m->sm_count, 8), 256, 0, m->stream>>>(
             m->ncols, m->colptr.as<long long>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(),
@@ -636,10 +696,6 @@ void prepare(rimdp_model* m) {
     int h[2] = {0, 0};
     CK(cudaMemcpyAsync(h, counters, sizeof h, cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
-    if (h[1]) {
-        fail(RIMDP_ERR_INVALID_ARGUMENT, "row index out of range [0, %d)", m->n_global);
-        throw Fail{RIMDP_ERR_INVALID_ARGUMENT};
-    }
     m->infeasible_cols.clear();
     if (h[0]) {
         std::vector<unsigned char> flags(m->ncols);
@@ -1583,6 +1639,7 @@ static int model_create_impl(const rimdp_model_desc* d, int state_begin, int num
         PhaseTrace tr("model_create");
         std::unique_ptr<rimdp_model> m(new rimdp_model);
         m->dtype = d->dtype;
+        m->col_offset = g_shard_col_offset;
         init_common(m.get(), d->device);
         tr.mark("init");
         DeviceGuard g(m->device);
@@ -2356,7 +2413,10 @@ int rimdp_multi_create(const rimdp_model_desc* d, int32_t world, const int32_t* 
             ld.lower = d->lower ? static_cast<const char*>(d->lower) + zb * es : nullptr;
             ld.upper = d->upper ? static_cast<const char*>(d->upper) + zb * es : nullptr;
             rimdp_model* m = nullptr;
-            if (int st = rimdp_model_create_shard(&ld, sb, n, &m)) return st;
+            g_shard_col_offset = cb; // violations found at upload name global columns
+            const int st = rimdp_model_create_shard(&ld, sb, n, &m);
+            g_shard_col_offset = 0;
+            if (st) return st;
             mm->shards.push_back(m);
             m->col_offset = cb;
             m->value_capacity = n;

@@ -122,10 +122,51 @@ prepare_columns(int ncols, const long long* __restrict__ colptr, const T* __rest
     }
 }
 
-__global__ void check_rows(long long nnz, const int* __restrict__ rows, int n, int* __restrict__ bad) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nnz; i += (long long)gridDim.x * blockDim.x) {
-        const int r = rows[i];
-        if (r < 0 || r >= n) atomicExch(bad, 1);
+// Device-side model validation at upload, in the
+// reference's report order: CscMatrix::structural_violation (csc.hpp:89-104:
+// per column, per entry: row in range, then strictly increasing rows) over
+// every column first, then IntervalProbabilities::validate's entry checks
+// (interval.hpp:148-164: per entry lower in [0,1] and finite, upper likewise,
+// lower <= upper).  One warp per column; the first violation of the model is
+// the minimum of (column, entry, check) keys, folded with atomicMin:
+//   first[0] structural: column << 32 | entry << 1 | (0 range, 1 order)
+//   first[1] entries:    column << 32 | entry << 2 | (0 lower, 1 upper, 2 order)
+// Runs before prepare_columns turns `upper` into gaps.
+template <class T>
+__global__ void __launch_bounds__(256)
+validate_entries(int ncols, const long long* __restrict__ colptr, const int* __restrict__ rows,
+                 const T* __restrict__ lower, const T* __restrict__ upper, int n, unsigned long long* __restrict__ first) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int c = blockIdx.x * 8 + w; c < ncols; c += gridDim.x * 8) {
+        const long long b = colptr[c], e = colptr[c + 1];
+        unsigned long long sk = ~0ull, ek = ~0ull;
+        int prev = 0;
+        for (long long j0 = b; j0 < e; j0 += 32) {
+            const long long j = j0 + lane;
+            const bool in = j < e;
+            const int r = in ? rows[j] : 0;
+            int before = __shfl_up_sync(kFull, r, 1);
+            if (lane == 0) before = prev;
+            prev = __shfl_sync(kFull, r, 31);
+            if (in) {
+                const unsigned long long pos = static_cast<unsigned long long>(j - b);
+                if (r < 0 || r >= n) sk = min(sk, (pos << 1) | 0ull);
+                else if (j > b && r <= before) sk = min(sk, (pos << 1) | 1ull);
+                const T l = lower[j], u = upper[j];
+                // !(0 <= x <= 1) is true for NaN; +-inf fail the range test too (Traits::is_finite)
+                if (!(l >= T(0) && l <= T(1))) ek = min(ek, (pos << 2) | 0ull);
+                else if (!(u >= T(0) && u <= T(1))) ek = min(ek, (pos << 2) | 1ull);
+                else if (l > u) ek = min(ek, (pos << 2) | 2ull); // the first check the reference pushes
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            sk = min(sk, __shfl_xor_sync(kFull, sk, o));
+            ek = min(ek, __shfl_xor_sync(kFull, ek, o));
+        }
+        if (lane == 0) {
+            if (sk != ~0ull) atomicMin(first, (static_cast<unsigned long long>(c) << 32) | sk);
+            if (ek != ~0ull) atomicMin(first + 1, (static_cast<unsigned long long>(c) << 32) | ek);
+        }
     }
 }
 

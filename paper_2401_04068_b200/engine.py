@@ -17,7 +17,10 @@ from . import build as _build
 
 RIMDP_F64, RIMDP_F32 = 0, 1
 (OK, ERR_INVALID_ARGUMENT, ERR_INFEASIBLE_COLUMN, ERR_NON_CONVERGENCE, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE, ERR_INTERNAL,
- ERR_MISSING_FILE, ERR_SCHEMA) = range(10)
+ ERR_MISSING_FILE, ERR_SCHEMA, ERR_INVALID_MODEL) = range(11)
+# rimdp::ViolationKind (reference errors.hpp:18-27)
+VIOLATION_KINDS = ("ShapeMismatch", "EntryOutOfRange", "BoundOrderViolation", "InfeasibleColumn",
+                   "DestinationCountMismatch", "DuplicateActionLabel", "EmptyActionSet", "StructuralError")
 
 
 class EngineError(RuntimeError):
@@ -29,12 +32,15 @@ class EngineError(RuntimeError):
         self.iterations = int(info.iterations)
         self.residual = float(info.residual)
         self.column = int(info.column)
+        self.violation_kind = int(info.violation_kind)
+        self.row = int(info.row)
         super().__init__(f"rimdp status {status}: {message}")
 
 
 class ErrorInfo(C.Structure):
     _fields_ = [("status", C.c_int32), ("iterations", C.c_int64), ("residual", C.c_double),
-                ("column", C.c_int64), ("infeasible_kind", C.c_int32), ("infeasible_sum", C.c_double)]
+                ("column", C.c_int64), ("infeasible_kind", C.c_int32), ("infeasible_sum", C.c_double),
+                ("violation_kind", C.c_int32), ("row", C.c_int64)]
 
 
 class ModelDesc(C.Structure):
