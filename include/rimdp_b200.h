@@ -184,6 +184,16 @@ int rimdp_native_read(const char* path, int32_t dtype, rimdp_native_sizes* sizes
 int rimdp_native_take(void* handle, int32_t* stateptr, int64_t* colptr, int32_t* rowval, void* lower, void* upper,
                       char* labels);
 void rimdp_native_free(void* handle);
+/* The engine's CSC arrays (rimdp_model_desc layout) as a container, like
+ * write_native_model (native.hpp:424-455).  index64 = 0: int32 column
+ * pointers when they fit (then the file is byte-identical to the
+ * reference's), int64 (variable dtype 6, an engine extension the reference's
+ * reader does not know) beyond 2^31-1 transitions; index64 = 1: always int64.
+ * labels: num_cols NUL-terminated action labels, or NULL for "0", "1", ...
+ * within each state. */
+int rimdp_native_write(const char* path, int32_t dtype, int32_t num_states, int32_t num_cols, const int32_t* stateptr,
+                       const int64_t* colptr, const int32_t* rowval, const void* lower, const void* upper,
+                       const char* labels, int32_t index64);
 
 /* ---- value iteration ---------------------------------------------------
  * One POD plan per solve, the marshalled form of detail::IterationPlan

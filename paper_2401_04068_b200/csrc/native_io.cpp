@@ -21,6 +21,13 @@
 //   * IntervalMDP::validate's structure checks (imdp.hpp:129-168).
 //   * the entry and column-sum checks of IntervalProbabilities::validate
 //     (interval.hpp:132-179) on the aligned pattern, before [0,0] removal.
+// 64-bit extension: the reference's int32 colptr caps a
+// container at 2^31-1 transitions (native.hpp:514-517), so BASELINE config 4
+// (5.12e9) cannot be stored.  Variables of dtype 6 = int64 are accepted for
+// lower_colptr / upper_colptr (the reference's reader rejects dtype 6 as
+// unknown, so such files are engine files); rimdp_native_write emits them
+// when the model needs them (or when asked), and int32 otherwise — then the
+// file is byte-identical to the reference's write_native_model.
 // Every failure is a SchemaViolation whose message is "schema violation:
 // <path>: <reason>" as in the reference (errors.hpp:92-95).  The JSON debug
 // variant of the container is not read here (text parsing is out of scope).
@@ -51,6 +58,7 @@ struct SchemaError : std::runtime_error {
 struct Var {
     uint8_t dtype = 0;
     std::vector<int32_t> i32;
+    std::vector<int64_t> i64; // dtype 6: 64-bit column pointers (engine extension)
     std::vector<double> f64;
     std::vector<float> f32;
     std::vector<std::string> str;
@@ -143,6 +151,7 @@ std::unique_ptr<Model<V>> read_model(const std::string& path) {
         if (v.count > (1ull << 33)) in.fail("variable " + key + " implausibly large");
         switch (v.dtype) {
         case 1: v.i32.resize(v.count); if (v.count) in.bytes(v.i32.data(), 4 * v.count); break;
+        case 6: v.i64.resize(v.count); if (v.count) in.bytes(v.i64.data(), 8 * v.count); break;
         case 2: v.f64.resize(v.count); if (v.count) in.bytes(v.f64.data(), 8 * v.count); break;
         case 3: v.f32.resize(v.count); if (v.count) in.bytes(v.f32.data(), 4 * v.count); break;
         case 4: v.str.resize(v.count); for (auto& s : v.str) s = in.str(); break;
@@ -196,9 +205,16 @@ std::unique_ptr<Model<V>> read_model(const std::string& path) {
         }
         return out;
     };
-    const std::vector<int32_t>& lcp = ints("lower_colptr");
+    // column pointers: int32 (the reference) or int64 (dtype 6)
+    auto ptrs = [&](const char* k) -> std::vector<int64_t> {
+        Var& v = var(k);
+        if (v.dtype == 1) return std::vector<int64_t>(v.i32.begin(), v.i32.end());
+        if (v.dtype == 6) return std::move(v.i64);
+        in.fail(std::string("variable ") + k + " must be int32 or int64");
+    };
+    const std::vector<int64_t> lcp = ptrs("lower_colptr");
     const std::vector<int32_t>& lrv = ints("lower_rowval");
-    const std::vector<int32_t>& ucp = ints("upper_colptr");
+    const std::vector<int64_t> ucp = ptrs("upper_colptr");
     const std::vector<int32_t>& urv = ints("upper_rowval");
     const std::vector<V> lnz = values("lower_nzval");
     const std::vector<V> unz = values("upper_nzval");
@@ -226,7 +242,7 @@ std::unique_ptr<Model<V>> read_model(const std::string& path) {
     for (int32_t r : urv)
         if (r < 0 || r >= ns) in.fail("IndexOutOfBounds: upper_rowval entry");
     // CscMatrix::from_csc -> structural_violation (csc.hpp:75-107); ModelError -> SchemaViolation
-    auto structural = [&](const std::vector<int32_t>& cp, const std::vector<int32_t>& rv, size_t nz) {
+    auto structural = [&](const std::vector<int64_t>& cp, const std::vector<int32_t>& rv, size_t nz) {
         const char* SE = "StructuralError";
         if (cp.front() != 0) in.model_error(SE, "colptr must start at 0");
         if (cp.back() != static_cast<int64_t>(rv.size()) || rv.size() != nz)
@@ -339,9 +355,137 @@ void take(const Model<V>& m, int32_t* sp, int64_t* cp, int32_t* rv, void* lo, vo
         }
 }
 
+// ---- writer: the engine's aligned CSC arrays -> an IMDPCSC1 container ------
+// Mirrors write_native_model (native.hpp:424-455) + write_container_binary
+// (:251-292): attributes and variables in key order (std::map), both bound
+// matrices with their zero entries stripped (IntervalProbabilities::lower_csc
+// / upper_csc, interval.hpp:125-129), stateptr and action labels.
+
+class Writer {
+public:
+    explicit Writer(const std::string& path) : path_(path), out_(path, std::ios::binary | std::ios::trunc) {
+        if (!out_) throw SchemaError(RIMDP_ERR_INVALID_ARGUMENT, "cannot open " + path + " for writing");
+    }
+    template <class U>
+    void le(U v) {
+        char b[sizeof(U)];
+        for (size_t i = 0; i < sizeof(U); ++i) b[i] = static_cast<char>((static_cast<uint64_t>(v) >> (8 * i)) & 0xff);
+        out_.write(b, sizeof(U));
+    }
+    void u8(uint8_t v) { out_.put(static_cast<char>(v)); }
+    void str(const std::string& s) {
+        le<uint32_t>(static_cast<uint32_t>(s.size()));
+        out_.write(s.data(), static_cast<std::streamsize>(s.size()));
+    }
+    template <class U>
+    void raw(const std::vector<U>& v) {
+        out_.write(reinterpret_cast<const char*>(v.data()), static_cast<std::streamsize>(sizeof(U) * v.size()));
+    }
+    void finish() {
+        out_.flush();
+        if (!out_) throw SchemaError(RIMDP_ERR_INVALID_ARGUMENT, "write to " + path_ + " failed");
+    }
+
+private:
+    std::string path_;
+    std::ofstream out_;
+};
+
+template <class V>
+void write_model(const char* path, int32_t ns, int32_t nc, const int32_t* sp, const int64_t* cp, const int32_t* rv,
+                 const V* lower, const V* upper, const char* labels, int32_t index64) {
+    // the two matrices, zero entries stripped
+    std::vector<int64_t> lcp{0}, ucp{0};
+    std::vector<int32_t> lrv, urv;
+    std::vector<V> lnz, unz;
+    for (int32_t c = 0; c < nc; ++c) {
+        for (int64_t k = cp[c]; k < cp[c + 1]; ++k) {
+            if (lower[k] != V(0)) { lrv.push_back(rv[k]); lnz.push_back(lower[k]); }
+            if (upper[k] != V(0)) { urv.push_back(rv[k]); unz.push_back(upper[k]); }
+        }
+        lcp.push_back(static_cast<int64_t>(lrv.size()));
+        ucp.push_back(static_cast<int64_t>(urv.size()));
+    }
+    const bool wide = index64 != 0 || lcp.back() > INT32_MAX || ucp.back() > INT32_MAX;
+    std::vector<std::string> labs;
+    if (labels) {
+        const char* q = labels;
+        for (int32_t c = 0; c < nc; ++c) {
+            labs.emplace_back(q);
+            q += labs.back().size() + 1;
+        }
+    } else { // positional labels "0", "1", ... within each state
+        for (int32_t st = 0; st < ns; ++st)
+            for (int32_t c = sp[st]; c < sp[st + 1]; ++c) labs.push_back(std::to_string(c - sp[st]));
+    }
+    Writer w(path);
+    w.raw(std::vector<char>{'I', 'M', 'D', 'P', 'C', 'S', 'C', '1'});
+    w.le<uint32_t>(5);
+    const std::pair<const char*, std::string> attrs[5] = {
+        {"cols", "from/action"}, {"format", "sparse_csc"}, {"model", "imdp"}, {"num_states", std::to_string(ns)},
+        {"rows", "to"}};
+    for (const auto& [k, v] : attrs) {
+        w.str(k);
+        w.str(v);
+    }
+    w.le<uint32_t>(8);
+    const uint8_t vdt = sizeof(V) == 8 ? 2 : 3;
+    auto ptr_var = [&](const char* key, const std::vector<int64_t>& p) {
+        w.str(key);
+        w.u8(wide ? 6 : 1);
+        w.le<uint64_t>(p.size());
+        if (wide) {
+            w.raw(p);
+        } else {
+            std::vector<int32_t> n(p.begin(), p.end());
+            w.raw(n);
+        }
+    };
+    auto var = [&](const char* key, uint8_t dt, const auto& v) {
+        w.str(key);
+        w.u8(dt);
+        w.le<uint64_t>(v.size());
+        w.raw(v);
+    };
+    w.str("action_vals");
+    w.u8(4);
+    w.le<uint64_t>(labs.size());
+    for (const auto& l : labs) w.str(l);
+    ptr_var("lower_colptr", lcp);
+    var("lower_nzval", vdt, lnz);
+    var("lower_rowval", 1, lrv);
+    var("stateptr", 1, std::vector<int32_t>(sp, sp + ns + 1));
+    ptr_var("upper_colptr", ucp);
+    var("upper_nzval", vdt, unz);
+    var("upper_rowval", 1, urv);
+    w.finish();
+}
+
 } // namespace
 
 extern "C" {
+
+int rimdp_native_write(const char* path, int32_t dtype, int32_t num_states, int32_t num_cols, const int32_t* stateptr,
+                       const int64_t* colptr, const int32_t* rowval, const void* lower, const void* upper,
+                       const char* labels, int32_t index64) {
+    if (!path || !stateptr || !colptr || num_states < 0 || num_cols < 0 || (dtype != RIMDP_F64 && dtype != RIMDP_F32) ||
+        (colptr[num_cols] > 0 && (!rowval || !lower || !upper)))
+        return rimdp_internal_fail(RIMDP_ERR_INVALID_ARGUMENT, "rimdp_native_write: bad argument");
+    try {
+        if (dtype == RIMDP_F64)
+            write_model<double>(path, num_states, num_cols, stateptr, colptr, rowval, static_cast<const double*>(lower),
+                                static_cast<const double*>(upper), labels, index64);
+        else
+            write_model<float>(path, num_states, num_cols, stateptr, colptr, rowval, static_cast<const float*>(lower),
+                               static_cast<const float*>(upper), labels, index64);
+        return RIMDP_OK;
+    } catch (const SchemaError& e) {
+        return rimdp_internal_fail(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return rimdp_internal_fail(RIMDP_ERR_OUT_OF_MEMORY, "host allocation failed");
+    }
+}
+
 
 int rimdp_native_read(const char* path, int32_t dtype, rimdp_native_sizes* sizes, void** handle) {
     if (!path || !sizes || !handle || (dtype != RIMDP_F64 && dtype != RIMDP_F32))

@@ -114,6 +114,7 @@ _SIGNATURES = {
     "rimdp_native_read": ([C.c_char_p, _I32, _VP, _VP], C.c_int),
     "rimdp_native_take": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
     "rimdp_native_free": ([_VP], None),
+    "rimdp_native_write": ([C.c_char_p, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP, C.c_char_p, _I32], C.c_int),
     "rimdp_exchange_export": ([_VP, _VP], C.c_int),
     "rimdp_exchange_connect": ([_VP, _I32, _I32, _VP], C.c_int),
     "rimdp_exchange_connect_local": ([_VP, _I32], C.c_int),
@@ -255,6 +256,21 @@ def read_native_model(path, dtype=np.float64):
         lib.rimdp_native_free(h)
     labels = [x.decode() for x in lab.raw[:sz.label_bytes].split(b"\0")[:-1]]
     return sp, cp, rv, lo, up, labels
+
+
+def write_native_model(path, stateptr, colptr, rowval, lower, upper, labels=None, index64=False):
+    """The engine's CSC arrays as an IMDPCSC1 container (rimdp_native_write; write_native_model,
+    io/native.hpp:424-455).  int64 column pointers (dtype 6) when index64 or beyond 2^31-1 transitions."""
+    lower = np.asarray(lower)
+    dt = lower.dtype
+    sp = np.ascontiguousarray(stateptr, np.int32)
+    cp = np.ascontiguousarray(colptr, np.int64)
+    rv = np.ascontiguousarray(rowval, np.int32)
+    lo = np.ascontiguousarray(lower, dt)
+    up = np.ascontiguousarray(upper, dt)
+    lab = None if labels is None else b"".join(x.encode() + b"\0" for x in labels)
+    _check(load().rimdp_native_write(os.fsencode(path), _dt(dt), len(sp) - 1, len(cp) - 1, _p(sp), _p(cp), _p(rv),
+                                     _p(lo), _p(up), lab, int(bool(index64))))
 
 
 def _dt(dtype) -> int:
