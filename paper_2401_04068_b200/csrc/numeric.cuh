@@ -108,6 +108,42 @@ __device__ __forceinline__ int ld_hint(const int* a, unsigned long long pol) {
     return v;
 }
 
+// 128-bit (64-bit) vector forms of ld_hint: E consecutive entries of one lane
+// in one load.  The caller guarantees the alignment (column offset % E == 0).
+__device__ __forceinline__ void ld_hint_vec(const double* a, unsigned long long pol, double (&v)[2]) {
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(a), "l"(pol));
+}
+__device__ __forceinline__ void ld_hint_vec(const double* a, unsigned long long pol, double (&v)[4]) {
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(a), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v[2]), "=d"(v[3]) : "l"(a + 2), "l"(pol));
+}
+__device__ __forceinline__ void ld_hint_vec(const float* a, unsigned long long pol, float (&v)[2]) {
+    asm("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v[0]), "=f"(v[1]) : "l"(a), "l"(pol));
+}
+__device__ __forceinline__ void ld_hint_vec(const float* a, unsigned long long pol, float (&v)[4]) {
+    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(a), "l"(pol));
+}
+__device__ __forceinline__ void ld_hint_vec(const int* a, unsigned long long pol, int (&v)[2]) {
+    asm("ld.global.nc.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(v[0]), "=r"(v[1]) : "l"(a), "l"(pol));
+}
+__device__ __forceinline__ void ld_hint_vec(const int* a, unsigned long long pol, int (&v)[4]) {
+    asm("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "l"(a), "l"(pol));
+}
+
+// Entries [j0, j0 + E) of a column (base pointer p, length L) into v: one
+// vector load when the run is whole and aligned, else guarded scalar loads.
+template <int E, class U>
+__device__ __forceinline__ void ld_run(const U* p, int j0, int L, bool aligned, unsigned long long pol, U (&v)[E]) {
+    if (aligned && j0 + E <= L) {
+        ld_hint_vec(p + j0, pol, v);
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = j0 + e < L ? ld_hint(p + j0 + e, pol) : U(0);
+    }
+}
+
 // Programmatic dependent launch: the kernels
 // of an iteration are launched with programmatic stream serialization, so a
 // kernel's blocks can become resident while its predecessor drains.  Every

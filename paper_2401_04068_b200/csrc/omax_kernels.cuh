@@ -526,7 +526,9 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
     constexpr int B = Sh::B, W = Sh::W, LEN = Sh::Len;
     pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
-    __shared__ T xs[W][B][LEN + 1];
+    // +2: rows stay 16-byte aligned for the vector product stores and lane t's sequential reads of row t
+    // still spread over the banks
+    __shared__ __align__(16) T xs[W][B][LEN + 2];
     const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gw = blockIdx.x * W + w, nw = gridDim.x * W;
@@ -559,58 +561,37 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
 
     long long bn = __shfl_sync(kFull, mbeg, 0), bnn = __shfl_sync(kFull, mbeg, 1);
     int Ln = __shfl_sync(kFull, mlen, 0), Lnn = __shfl_sync(kFull, mlen, 1);
+    // lane l owns the E consecutive entries [l E, l E + E) of a column: one 64/128-bit load per array when
+    // the column starts on an E-entry boundary (config 4: always)
+    const int j0 = lane * E;
     int rowA[E], rowB[E];
     T lc[E], gc[E], vc[E], ln[E], gn[E], vn[E];
+    ld_run<E>(rows + bn, j0, Ln, (bn & (E - 1)) == 0, pstream, rowA);
+    ld_run<E>(lower + bn, j0, Ln, (bn & (E - 1)) == 0, pstream, lc);
+    ld_run<E>(gap + bn, j0, Ln, (bn & (E - 1)) == 0, pstream, gc);
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int j = e * 32 + lane;
-        rowA[e] = j < Ln ? ld_hint(rows + bn + j, pstream) : 0;
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int j = e * 32 + lane;
-        lc[e] = gc[e] = vc[e] = T(0);
-        if (j < Ln) {
-            lc[e] = ld_hint(lower + bn + j, pstream);
-            gc[e] = ld_hint(gap + bn + j, pstream);
-            vc[e] = ld_hint(V + rowA[e], pval);
-        }
-    }
+    for (int e = 0; e < E; ++e) vc[e] = j0 + e < Ln ? ld_hint(V + rowA[e], pval) : T(0);
     int Lc = Ln;
     bn = bnn;
     Ln = Lnn;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int j = e * 32 + lane;
-        rowA[e] = j < Ln ? ld_hint(rows + bn + j, pstream) : 0;
-    }
+    ld_run<E>(rows + bn, j0, Ln, (bn & (E - 1)) == 0, pstream, rowA);
     bnn = __shfl_sync(kFull, mbeg, 2);
     Lnn = __shfl_sync(kFull, mlen, 2);
 
     for (;;) {
         for (int s = 0; s < B; ++s) {
+            ld_run<E>(lower + bn, j0, Ln, (bn & (E - 1)) == 0, pstream, ln);
+            ld_run<E>(gap + bn, j0, Ln, (bn & (E - 1)) == 0, pstream, gn);
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int j = e * 32 + lane;
-                ln[e] = gn[e] = vn[e] = T(0);
-                if (j < Ln) {
-                    ln[e] = ld_hint(lower + bn + j, pstream);
-                    gn[e] = ld_hint(gap + bn + j, pstream);
-                    vn[e] = ld_hint(V + rowA[e], pval);
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int j = e * 32 + lane;
-                rowB[e] = j < Lnn ? ld_hint(rows + bnn + j, pstream) : 0;
-            }
+            for (int e = 0; e < E; ++e) vn[e] = j0 + e < Ln ? ld_hint(V + rowA[e], pval) : T(0);
+            ld_run<E>(rows + bnn, j0, Lnn, (bnn & (E - 1)) == 0, pstream, rowB);
             // greedy O-max of column s (omax.hpp:98-112)
             const T r = __shfl_sync(kFull, mrem, s);
             Bits key[E];
             T p[E];
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                key[e] = e * 32 + lane < Lc ? order_key<T>(vc[e], kPess) : ~Bits(0);
+                key[e] = j0 + e < Lc ? order_key<T>(vc[e], kPess) : ~Bits(0);
                 p[e] = lc[e];
             }
             T consumed = T(0), avail = r;
@@ -635,8 +616,9 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
                     const unsigned mk = __reduce_min_sync(kFull, static_cast<unsigned>(bk));
                     cand = static_cast<unsigned>(bk) == mk;
                 }
-                const unsigned pos = __reduce_min_sync(kFull, cand ? static_cast<unsigned>(be * 32 + lane) : 0xffffffffu);
-                const int sel_lane = static_cast<int>(pos & 31u), sel_e = static_cast<int>(pos >> 5);
+                // ties of the key go to the lowest position = row (csc.hpp:98-101)
+                const unsigned pos = __reduce_min_sync(kFull, cand ? static_cast<unsigned>(j0 + be) : 0xffffffffu);
+                const int sel_lane = static_cast<int>(pos / E), sel_e = static_cast<int>(pos % E);
                 T mine = gc[0];
 #pragma unroll
                 for (int e = 1; e < E; ++e)
@@ -653,9 +635,17 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
                 consumed = N::add(consumed, gs);
                 avail = N::sub(r, consumed);
             }
+            {
+                T x[E];
 #pragma unroll
-            for (int e = 0; e < E; ++e)
-                if (e * 32 + lane < Lc) xs[w][s][e * 32 + lane] = N::mul(vc[e], p[e]);
+                for (int e = 0; e < E; ++e) x[e] = N::mul(vc[e], p[e]); // entries past the column are never read
+                if constexpr (E == 2 && sizeof(T) == 8) {
+                    *reinterpret_cast<double2*>(&xs[w][s][j0]) = make_double2(x[0], x[1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) xs[w][s][j0 + e] = x[e];
+                }
+            }
             // rotate the pipeline
 #pragma unroll
             for (int e = 0; e < E; ++e) {
