@@ -110,9 +110,10 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
         if (tid == 0) {
             kmin_s = ~0u;
             kmax_s = 0u;
-            over = 0;
         }
         __syncthreads();
+        // every read of the previous column's flag happened before the barrier above (racecheck-clean)
+        if (tid == 0) over = 0;
         unsigned key[E];
         float g[E];
         unsigned lmin = ~0u, lmax = 0u;
@@ -185,7 +186,9 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
             }
         }
         __syncthreads();
-        if (tid == 0 && over) fb_list[atomicAdd(fb_count, 1)] = c;
+        if (tid == 0) {
+            if (over) fb_list[atomicAdd(fb_count, 1)] = c;
+        }
     }
 }
 
