@@ -271,17 +271,47 @@ exact_dot(int nlist, const int* __restrict__ list, const long long* __restrict__
             const int j = u * 32 + lane;
             gv[u] = j < L ? S[b0 + j] : 0.f;
         }
+        // exact (f64) sum of the sorted gaps walked so far: the chunk sums of <= 128 float32 gaps of one column
+        // are exact in double
+        double P = 0.0;
         for (int j0 = 0; j0 < L; j0 += 128) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) sb[u * 32 + lane] = gv[u];
+            double cs = (double)gv[0] + (double)gv[1] + (double)gv[2] + (double)gv[3];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int j = j0 + 128 + u * 32 + lane;
                 gn[u] = j < L ? S[b0 + j] : 0.f;
             }
-            __syncwarp();
-            int picks = 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(kFull, cs, o);
             const int m = L - j0 < 128 ? L - j0 : 128;
+            // fast chunk: the sequential float32 `consumed` after any entry of the chunk is at most the exact
+            // prefix times (1 + 1.01 (j0 + m) 2^-24) (positive terms); below rem it stays below rem, so every
+            // entry is a full pick (extra = gap, already in S) and the walk continues: only the chain runs
+            P += cs;
+            const bool fast = P * (1.0 + 1.02 * (double)(j0 + m) * 0x1p-24) < (double)r; // 2% slack: f64 rounding of P
+            __syncwarp();
+            int picks = m;
+            if (fast) {
+                if (lane == 0) {
+                    const float4* s4 = reinterpret_cast<const float4*>(sb);
+                    const int m4 = m >> 2;
+#pragma unroll 8
+                    for (int k = 0; k < m4; ++k) {
+                        const float4 g4 = s4[k];
+                        consumed = N_::add(consumed, g4.x);
+                        consumed = N_::add(consumed, g4.y);
+                        consumed = N_::add(consumed, g4.z);
+                        consumed = N_::add(consumed, g4.w);
+                    }
+                    for (int k = m4 * 4; k < m; ++k) consumed = N_::add(consumed, sb[k]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) gv[u] = gn[u];
+                __syncwarp();
+                continue;
+            }
             if (lane == 0) picks = exact_walk_chunk(sb, m, r, consumed);
             picks = __shfl_sync(kFull, picks, 0);
             __syncwarp();
