@@ -71,15 +71,20 @@ def log(*a):
 def scaled_workload(w, world, scaling):
     """The workload at `world` GPUs.  Weak scaling (the default for C2, the
     default config): the same law with world x the states, so every GPU
-    keeps C2's 100000 states x 4 actions x 32 successors (density 32 / n).
-    Configs 3-5 are fixed-size (C4 is already the 8-GPU shard config):
+    keeps C2's 100000 states x 4 actions x 32 successors.  At N > 1 the
+    columns come from the counter generator with random_imdp's value law
+    (lower = u/32, upper = min(lower + v (1 - 1/32), 1)), each rank
+    generating only its own shard in HBM — random_imdp's sequential
+    mt19937_64 stream would make every rank build the whole N x model on the
+    host.  Configs 3-5 are fixed-size (C4 is already the 8-GPU shard config):
     strong scaling."""
     if scaling == "weak" and world > 1 and w.get("weak_support"):
         n = w["states"] * world
-        w = dict(w, states=n, density=w["weak_support"] / n,
-                 desc=w["desc"].split(":")[0] + f" weak-scaled x{world}: random_imdp {n} states x {w['actions']} "
-                      f"actions x {w['weak_support']} successors, Pmaxmin InfiniteTimeReachability(goal = last 1%, "
-                      "eps = 1e-6)")
+        k = w["weak_support"]
+        w = dict(w, states=n, source="generated", law=0, support=k, sample=dict(states=w["states"]),
+                 desc=w["desc"].split(":")[0] + f" law weak-scaled x{world}: {n} states x {w['actions']} actions x "
+                      f"{k} successors (counter generator, random_imdp's value law; each rank generates its shard "
+                      "in HBM), Pmaxmin InfiniteTimeReachability(goal = last 1%, eps = 1e-6)")
         return w, "weak"
     return w, ("weak" if (w.get("weak_support") and scaling == "weak") else "strong")
 
