@@ -433,7 +433,11 @@ def engine_arm(args, w):
                      "phase_ms": {"fused_short_states": fused_avg, "column_kernels": cols_avg,
                                   "action_kernel": act_avg},
                      "kernel_share_of_step": kernel_avg / max(fused_avg + cols_avg + act_avg, 1e-12),
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     # the same phase against its measured DRAM bytes (ncu, cold cache): below the algorithmic
+                     # fraction when V gathers hit L2 (C2, C3: V in L2 / shared memory), above when they miss (C4)
+                     "dram_achieved": (traffic / (kernel_avg * 1e-3) / 1e9) if traffic else None,
+                     "dram_frac": (traffic / (kernel_avg * 1e-3) / 1e9 / peak) if traffic else None},
         "e2e": {"value": total_nnz * e2e_iters / e2e_s, "unit": "transitions/s",
                 "h2d_bytes_per_step": h2d / max(e2e_iters, 1), "d2h_bytes_per_step": d2h / max(e2e_iters, 1),
                 "seconds_to_convergence": e2e_s, "iterations": e2e_iters,
