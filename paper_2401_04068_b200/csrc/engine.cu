@@ -918,7 +918,34 @@ FallbackSlots fallback_slots(rimdp_model* m, int cls, int count) {
 
 template <class T, bool P, int LG>
 void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
-    if constexpr (std::is_same<T, float>::value) {
+    if constexpr (std::is_same<T, float>::value && LG <= 8) {
+        // <= 256 entries: one pass per column, one warp (exact_warp)
+        using Sh = ExactWarpShape<LG>;
+        auto k = exact_warp<P, LG>;
+        static bool configured[64] = {};
+        static int per_sm[64] = {};
+        const int dev = m->device & 63;
+        if (!configured[dev]) {
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem()));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, Sh::W * 32, Sh::smem()));
+            per_sm[dev] = std::max(per_sm[dev], 1);
+            configured[dev] = true;
+        }
+        const FallbackSlots f = fallback_slots(m, LG - kSortedMinLog, count);
+        launch_pdl(m->pdl_now, k, grid_for(count, Sh::W, m->sm_count, per_sm[dev]), Sh::W * 32, Sh::smem(), m->ls,
+                   count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(),
+                   m->gap.as<float>(), m->rem.as<float>(), V, q, f.list, f.count, f.other, (const Ctl*)ctl);
+        using SS = SortedShape<LG>;
+        auto kf = omax_sorted<float, P, LG, true>;
+        static bool fconf[64] = {};
+        if (!fconf[dev]) {
+            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::template smem<float>()));
+            fconf[dev] = true;
+        }
+        launch_pdl(m->pdl_now, kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
+                   (const int*)f.list, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(),
+                   m->gap.as<float>(), m->rem.as<float>(), V, q, (const Ctl*)ctl, (const int*)f.count);
+    } else if constexpr (std::is_same<T, float>::value) {
         using Sh = ExactShape<LG>;
         auto ks = exact_sort<P, LG>;
         static bool configured[64] = {};

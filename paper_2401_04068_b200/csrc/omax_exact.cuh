@@ -376,4 +376,210 @@ exact_dot(int nlist, const int* __restrict__ list, const long long* __restrict__
     }
 }
 
+// ---------------------------------------------------------------------------
+// Columns of 33 .. 256 entries in one pass, one warp per column
+// (exact_warp): the same sort, greedy walk and row-order dot as exact_sort +
+// exact_dot, but everything stays in the warp's shared-memory slice — no
+// block barriers, no global scratch, no second launch.  For these short
+// classes the two-pass route paid its per-column fixed costs twice (29 ns
+// per transition on C5 f32 against ~8 for the long classes).
+template <int LG>
+struct ExactWarpShape {
+    static constexpr int N = 1 << LG;   // 64 .. 256
+    static constexpr int E = N / 32;    // entries per lane
+    static constexpr int W = 8;         // warps per block
+    // per warp: tmp u64[N] (then the dot's staging buffer) | cnt u32[N + 4] | S f32[N]; each lane keeps its
+    // entries' V, lower, gap and sorted position in registers
+    static constexpr size_t warp_bytes = (size_t)N * 8 + (size_t)(N + 4) * 4 + (size_t)N * 4;
+    static constexpr size_t smem() { return W * ((warp_bytes + 15) / 16 * 16); }
+};
+
+template <bool kPess, int LG>
+__global__ void __launch_bounds__(ExactWarpShape<LG>::W * 32)
+exact_warp(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+           const int* __restrict__ rows, const float* __restrict__ lower, const float* __restrict__ gap,
+           const float* __restrict__ rem, const float* __restrict__ V, float* __restrict__ q,
+           int* __restrict__ fb_list, int* __restrict__ fb_count, int* __restrict__ fb_other,
+           const Ctl* __restrict__ ctl) {
+    using Sh = ExactWarpShape<LG>;
+    using N_ = Num<float>;
+    constexpr int N = Sh::N, E = Sh::E, W = Sh::W;
+    pdl_enter();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) *fb_other = 0; // the other parity's count (see exact_sort)
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned char* base = smem_raw + (size_t)w * ((Sh::warp_bytes + 15) / 16 * 16);
+    unsigned long long* tmp = reinterpret_cast<unsigned long long*>(base);
+    float* xb = reinterpret_cast<float*>(base);                       // dot staging, after the sort
+    unsigned* cnt = reinterpret_cast<unsigned*>(base + (size_t)N * 8);
+    float* S = reinterpret_cast<float*>(base + (size_t)N * 8 + (size_t)(N + 4) * 4);
+    for (int item = blockIdx.x * W + w; item < nlist; item += gridDim.x * W) {
+        const int c = list[item];
+        const long long b0 = colptr[c];
+        const int L = static_cast<int>(colptr[c + 1] - b0);
+        const float r = rem[c];
+        // ---- load, keys, the column's value range ----
+        unsigned key[E];
+        float g[E], v[E], lo[E];
+        float wlo = 3.0e38f, whi = -3.0e38f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = lane + 32 * e;
+            key[e] = ~0u;
+            g[e] = v[e] = lo[e] = 0.f;
+            if (j < L) {
+                v[e] = __ldg(V + __ldg(rows + b0 + j));
+                g[e] = __ldg(gap + b0 + j);
+                lo[e] = __ldg(lower + b0 + j);
+                key[e] = static_cast<unsigned>(order_key<float>(v[e], kPess));
+                const float wv = kPess ? __fadd_rn(v[e], 0.f) : -__fadd_rn(v[e], 0.f);
+                wlo = fminf(wlo, wv);
+                whi = fmaxf(whi, wv);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wlo = fminf(wlo, __shfl_xor_sync(kFull, wlo, o));
+            whi = fmaxf(whi, __shfl_xor_sync(kFull, whi, o));
+        }
+        const float width = __fsub_rn(whi, wlo);
+        const float scale = width > 0.f && width < 3.0e38f ? __fdiv_rn(static_cast<float>(N), width) : 0.f;
+        // ---- counting sort by (key, position): N buckets of the value range, then ranks inside buckets ----
+#pragma unroll
+        for (int e = 0; e < (N + 4) / 32 + 1; ++e)
+            if (lane + 32 * e < N + 4) cnt[lane + 32 * e] = 0u;
+        __syncwarp();
+        int bk[E];
+        unsigned slot[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = lane + 32 * e;
+            bk[e] = 0;
+            slot[e] = 0;
+            if (j < L) {
+                const float wv = kPess ? __fadd_rn(v[e], 0.f) : -__fadd_rn(v[e], 0.f);
+                const float x = __fmul_rn(__fsub_rn(wv, wlo), scale);
+                bk[e] = x < static_cast<float>(N - 1) ? static_cast<int>(x) : N - 1;
+                slot[e] = atomicAdd(&cnt[bk[e]], 1u);
+            }
+        }
+        __syncwarp();
+        {   // exclusive scan of cnt[0 .. N): lane l owns counters [l E, l E + E)
+            unsigned cv[E], run = 0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                cv[e] = cnt[lane * E + e];
+                run += cv[e];
+            }
+            unsigned incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            unsigned bse = incl - run;
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                cnt[lane * E + e] = bse;
+                bse += cv[e];
+            }
+            if (lane == 31) cnt[N] = bse;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = lane + 32 * e;
+            if (j < L) tmp[cnt[bk[e]] + slot[e]] = (static_cast<unsigned long long>(key[e]) << 13) | j;
+        }
+        __syncwarp();
+        bool over = false;
+        int sp[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = lane + 32 * e;
+            sp[e] = N;
+            if (j < L) {
+                const unsigned s0 = cnt[bk[e]], s1 = cnt[bk[e] + 1];
+                if (s1 - s0 > static_cast<unsigned>(kExactMaxBucket)) {
+                    over = true;
+                } else {
+                    const unsigned long long mine = (static_cast<unsigned long long>(key[e]) << 13) | j;
+                    unsigned rk = 0;
+                    for (unsigned k = s0; k < s1; ++k) rk += tmp[k] < mine;
+                    sp[e] = static_cast<int>(s0 + rk);
+                    S[sp[e]] = g[e];
+                }
+            }
+        }
+        if (__any_sync(kFull, over)) { // heavy ties: the bitonic exact kernel takes the column
+            if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = c;
+            __syncwarp();
+            continue;
+        }
+        __syncwarp();
+        // ---- the greedy (omax.hpp:102-110) along S, provably-full chunks as in exact_dot ----
+        float consumed = 0.f;
+        int J = L;
+        double P = 0.0;
+        for (int j0 = 0; j0 < L; j0 += 128) {
+            const int m = L - j0 < 128 ? L - j0 : 128;
+            double cs = 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = u * 32 + lane;
+                cs += k < m ? (double)S[j0 + k] : 0.0;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(kFull, cs, o);
+            P += cs;
+            const bool fast = P * (1.0 + 1.02 * (double)(j0 + m) * 0x1p-24) < (double)r;
+            int picks = m;
+            if (lane == 0) {
+                if (fast) {
+                    for (int k = 0; k < m; ++k) consumed = N_::add(consumed, S[j0 + k]);
+                } else {
+                    picks = exact_walk_chunk(S + j0, m, r, consumed);
+                }
+            }
+            picks = __shfl_sync(kFull, picks, 0);
+            __syncwarp();
+            if (picks < m) {
+                J = j0 + picks;
+                break;
+            }
+        }
+        // ---- row-order expectation (omax.hpp:169-173): 32 products staged, lane 0 adds them in order ----
+        float dot = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i0 = 32 * e;
+            if (i0 >= L) break;
+            // entry i0 + lane is this lane's entry e: its V, lower and sorted position are in registers
+            xb[lane] = lane + i0 < L ? N_::mul(v[e], sp[e] < J ? N_::add(lo[e], S[sp[e]]) : lo[e]) : 0.f;
+            __syncwarp();
+            if (lane == 0) {
+                const int m = L - i0 < 32 ? L - i0 : 32;
+                if (m == 32) {
+                    const float4* x4 = reinterpret_cast<const float4*>(xb);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float4 y = x4[k];
+                        dot = N_::add(dot, y.x);
+                        dot = N_::add(dot, y.y);
+                        dot = N_::add(dot, y.z);
+                        dot = N_::add(dot, y.w);
+                    }
+                } else {
+                    for (int k = 0; k < m; ++k) dot = N_::add(dot, xb[k]);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) q[c] = dot;
+        __syncwarp();
+    }
+}
+
 } // namespace rimdp_dev
