@@ -25,6 +25,30 @@ def bits(a):
     return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
 
 
+def f32_ulps(q, ref):
+    """Distance of float32 results from the reference, in units of the reference's last place."""
+    ref = np.asarray(ref, np.float32)
+    return np.abs(np.asarray(q, np.float64) - ref.astype(np.float64)) / np.spacing(np.abs(ref)).astype(np.float64)
+
+
+# tree-order float32 sums (RIMDP_F32_FAST / RIMDP_LONG=select) against the reference's sequential ones over
+# columns of up to 8192 entries: both carry rounding error of up to ~L/2 * 2^-24 relative (the reference's
+# sequential sum is the less accurate one); measured at most 57 ulps here
+F32_TREE_ULPS = 128
+
+
+def with_env(name, value, fn):
+    old = os.environ.get(name)
+    os.environ[name] = value
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[name]
+        else:
+            os.environ[name] = old
+
+
 def with_long_mode(mode, fn):
     old = os.environ.get("RIMDP_LONG")
     os.environ["RIMDP_LONG"] = mode
@@ -98,13 +122,14 @@ def test_select_random_values_within_tolerance(powerlaw, pess):
     v32 = v.astype(np.float32)
     ref32 = ref_columns(arr32, v32, pess)
     q32 = with_long_mode("select", lambda: engine.DeviceModel.from_csc(*arr32)).column_values(v32, pess)
-    assert np.abs(q32.astype(np.float64) - ref32).max() <= 1e-5
+    assert f32_ulps(q32, ref32).max() <= F32_TREE_ULPS
 
 
 @pytest.mark.parametrize("pess", [True, False])
 def test_default_random_values_within_tolerance(powerlaw, pess):
-    """Default routing (value buckets: omax_bucket for > 256 entries,
-    omax_wbucket for 33-256) on continuous values, f64 and f32; deterministic."""
+    """Default routing on continuous values, deterministic.  float64: value buckets (omax_bucket for > 256
+    entries, omax_wbucket for 33-256), within 1e-13.  float32: the exact route (exact_warp / exact_sort +
+    exact_dot), bit-identical; with RIMDP_F32_FAST=1 the value buckets, within a few ulps."""
     v = np.random.default_rng(9).random(9000)
     ref = ref_columns(powerlaw, v, pess)
     m = engine.DeviceModel.from_csc(*powerlaw)
@@ -116,7 +141,9 @@ def test_default_random_values_within_tolerance(powerlaw, pess):
     v32 = v.astype(np.float32)
     ref32 = ref_columns(arr32, v32, pess)
     q32 = engine.DeviceModel.from_csc(*arr32).column_values(v32, pess)
-    assert np.abs(q32.astype(np.float64) - ref32).max() <= 1e-5
+    assert np.array_equal(bits(q32), bits(ref32.astype(np.float32)))
+    fast = with_env("RIMDP_F32_FAST", "1", lambda: engine.DeviceModel.from_csc(*arr32)).column_values(v32, pess)
+    assert f32_ulps(fast, ref32).max() <= F32_TREE_ULPS
 
 
 @pytest.mark.parametrize("pess", [True, False])
@@ -253,12 +280,15 @@ def test_single_pass_long_kernel_within_tolerance(fewpick, pess, values):
 
 @pytest.mark.parametrize("pess", [True, False])
 def test_single_pass_long_kernel_f32(fewpick, pess):
-    """The f32 store of the same few-pick columns (NumericTraits<float>, tol 1e-5)."""
+    """The f32 store of the same few-pick columns: the default float32 route is row-order (omax_long),
+    bit-identical; the tree-order kernel (RIMDP_F32_FAST=1) within a few ulps."""
     sp, cp, rv, lo, up = fewpick
     arr32 = (sp, cp, rv, lo.astype(np.float32), up.astype(np.float32))
     v32 = np.random.default_rng(10).random(400).astype(np.float32)
     ref32 = ref_columns(arr32, v32, pess)
     q32 = engine.DeviceModel.from_csc(*arr32).column_values(v32, pess)
-    assert np.abs(q32.astype(np.float64) - ref32).max() <= 1e-5
+    assert np.array_equal(bits(q32), bits(ref32.astype(np.float32)))
+    fast = with_env("RIMDP_F32_FAST", "1", lambda: engine.DeviceModel.from_csc(*arr32)).column_values(v32, pess)
+    assert f32_ulps(fast, ref32).max() <= F32_TREE_ULPS
     ex = with_long_mode("exact", lambda: engine.DeviceModel.from_csc(*arr32))
     assert np.array_equal(bits(ex.column_values(v32, pess)), bits(ref32.astype(np.float32)))
