@@ -245,7 +245,9 @@ int rimdp_solve_finish(rimdp_model* model, const rimdp_outputs* out);
  * on the model stream around its three phases: the fused short-state kernel,
  * the per-column kernels of the remaining states, and their action kernel.
  * profile_read synchronises, returns the summed milliseconds of each phase
- * and the iteration count since the last read, and resets the accumulators. */
+ * and the iteration count since the last read, and resets the accumulators;
+ * kernels_per_iteration is the number of kernels the last enqueued iteration
+ * launched (every class kernel, fallback pass, range pass and stop test). */
 int rimdp_profile_enable(rimdp_model* model, int32_t on);
 int rimdp_profile_read(rimdp_model* model, double* fused_ms, double* columns_ms, double* action_ms,
                        int64_t* iterations, int32_t* kernels_per_iteration);

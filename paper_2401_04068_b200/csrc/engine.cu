@@ -161,6 +161,7 @@ struct SolveState {
     double eps = 0, discount = 0;
     int chosen_td = 0;
     long long launched = 0; // iterations enqueued so far
+    int launches_last = 0;  // kernels the last enqueued iteration launched (gpu_launches in bench.py)
     bool active = false;
     bool record_only = false;
     // kernel timing (rimdp_profile_*)
@@ -385,9 +386,14 @@ bool pdl_enabled() {
     return on;
 }
 
+// Kernel launches issued by this thread (every launch of the iteration loop goes through launch_pdl or
+// counts itself), so launch_iteration can report how many kernels one iteration really launched.
+thread_local long long g_launches = 0;
+
 template <class... KArgs, class... Args>
 void launch_pdl(bool on, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                 Args&&... args) {
+    ++g_launches;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -1234,6 +1240,7 @@ void launch_value_range(rimdp_model* m, const ColumnLists& L, const T* V) {
     m->vrange_parity ^= 1;
     const int n = m->n_global;
     value_range<T><<<grid_for(n, 256 * 8, m->sm_count, 4), 256, 0, m->stream>>>(n, V, slot, other);
+    ++g_launches;
     m->vrange_cur = slot;
 }
 
@@ -1278,6 +1285,7 @@ constexpr int kPdlMaxKernels = 3;
 template <class T>
 void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     SolveState& s = m->s;
+    const long long launches0 = g_launches;
     const T* vin = static_cast<const T*>(s.vb[(k - 1) & 1]);
     T* vout = static_cast<T*>(s.vb[k & 1]);
     Ctl* ctl = s.ctl.as<Ctl>();
@@ -1342,9 +1350,11 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
         // the global stop test once every rank has published iteration k (peer_sync_stop)
         peer_sync_stop<T><<<1, 32, 0, m->stream>>>(ctl, m->x.table.as<PeerTable>(), k, s.finite, s.horizon,
                                                    std::max(1LL, s.max_iterations), (T)s.eps);
+        ++g_launches;
     }
     if (ev) CK(cudaEventRecord(ev[3], m->stream));
     m->pdl_now = false;
+    s.launches_last = (int)(g_launches - launches0);
     CK(cudaGetLastError());
 }
 
@@ -1861,7 +1871,7 @@ int rimdp_profile_read(rimdp_model* m, double* fused_ms, double* columns_ms, dou
         if (columns_ms) *columns_ms = c;
         if (action_ms) *action_ms = a;
         if (iterations) *iterations = it;
-        if (kernels) *kernels = kernels_per_iteration(m);
+        if (kernels) *kernels = m->s.launches_last > 0 ? m->s.launches_last : kernels_per_iteration(m);
         return RIMDP_OK;
     });
 }
