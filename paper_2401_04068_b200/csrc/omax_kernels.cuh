@@ -272,7 +272,8 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
     using Bits = typename N::Bits;
     pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
-    __shared__ T xs[kWarpsPerBlock][kShortBatch][kShortLen + 1];
+    // +2: 16-byte aligned rows for the paired loads of the row-order sums, still spread over the banks
+    __shared__ __align__(16) T xs[kWarpsPerBlock][kShortBatch][kShortLen + 2];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
     // batches: the first one static, the rest handed out by a work counter
@@ -336,21 +337,22 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
             const T r = __shfl_sync(kFull, mrem, s);
             const bool valid = lane < Lc;
             Bits key = valid ? order_key<T>(vc, kPess) : ~Bits(0);
-            T p = lc;
             T consumed = T(0);
             T avail = r;
+            T mine = T(-1); // the avail at this lane's pick (picks only happen with avail > 0)
             for (int nsel = 0; avail > T(0) && nsel < Lc; ++nsel) {
                 const int sel = warp_argmin_sentinel(key);
                 const T gs = __shfl_sync(kFull, gc, sel);
-                {   // branch-free winner update (a divergent branch costs more than the DADD)
+                {   // branch-free winner update; the winner's share is formed once, after the loop
                     const bool me = lane == sel;
-                    const T pn = N::add(lc, gc < avail ? gc : avail);
-                    p = me ? pn : p;
+                    mine = me ? avail : mine;
                     key = me ? ~Bits(0) : key;
                 }
                 consumed = N::add(consumed, gs);
                 avail = N::sub(r, consumed);
             }
+            // omax.hpp:107: p = lower + (gap < avail ? gap : avail) for a picked position, lower otherwise
+            const T p = mine > T(0) ? N::add(lc, gc < mine ? gc : mine) : lc;
             if (valid) xs[w][s][lane] = N::mul(vc, p);
             // rotate the pipeline; metadata of column i+3 = window lane s+3
             lc = ln;
@@ -367,7 +369,16 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
         __syncwarp();
         if (lane < kShortBatch && mc >= 0) {
             T acc = T(0);
-            for (int i = 0; i < mlen; ++i) acc = N::add(acc, xs[w][lane][i]);
+            int i = 0;
+            if constexpr (sizeof(T) == 8) {
+                const double2* x2 = reinterpret_cast<const double2*>(xs[w][lane]);
+                for (; i + 2 <= mlen; i += 2) {
+                    const double2 y = x2[i >> 1];
+                    acc = N::add(acc, y.x);
+                    acc = N::add(acc, y.y);
+                }
+            }
+            for (; i < mlen; ++i) acc = N::add(acc, xs[w][lane][i]);
             q[mc] = acc;
         }
         __syncwarp();
