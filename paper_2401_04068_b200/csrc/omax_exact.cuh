@@ -538,7 +538,16 @@ exact_warp(int nlist, const int* __restrict__ list, const long long* __restrict_
             int picks = m;
             if (lane == 0) {
                 if (fast) {
-                    for (int k = 0; k < m; ++k) consumed = N_::add(consumed, S[j0 + k]);
+                    const float4* s4 = reinterpret_cast<const float4*>(S + j0);
+                    int k = 0;
+                    for (; k + 4 <= m; k += 4) {
+                        const float4 g4 = s4[k >> 2];
+                        consumed = N_::add(consumed, g4.x);
+                        consumed = N_::add(consumed, g4.y);
+                        consumed = N_::add(consumed, g4.z);
+                        consumed = N_::add(consumed, g4.w);
+                    }
+                    for (; k < m; ++k) consumed = N_::add(consumed, S[j0 + k]);
                 } else {
                     picks = exact_walk_chunk(S + j0, m, r, consumed);
                 }
