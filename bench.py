@@ -60,7 +60,7 @@ WORKLOADS = {
                     "eps = 1e-6",
                source="generated", states=1_000_000, actions=4, law=1, alpha=1.5, kmax=4096, seed=1,
                kind="reward", discount=0.95, pessimistic=True, maximize=True, eps=1e-6,
-               sample=dict(states=50_000)),
+               sample=dict(states=50_000), host_arrays=True),
 }
 
 
@@ -81,10 +81,10 @@ def scaled_workload(w, world, scaling):
     if scaling == "weak" and world > 1 and w.get("weak_support"):
         n = w["states"] * world
         k = w["weak_support"]
-        w = dict(w, states=n, source="generated", law=0, support=k, sample=dict(states=w["states"]),
+        w = dict(w, states=n, source="generated", law=0, support=k, sample=dict(states=w["states"]), host_arrays=True,
                  desc=w["desc"].split(":")[0] + f" law weak-scaled x{world}: {n} states x {w['actions']} actions x "
-                      f"{k} successors (counter generator, random_imdp's value law; each rank generates its shard "
-                      "in HBM), Pmaxmin InfiniteTimeReachability(goal = last 1%, eps = 1e-6)")
+                      f"{k} successors (counter generator, random_imdp's value law; each rank generates only its "
+                      "shard, on the host, and uploads it), Pmaxmin InfiniteTimeReachability(goal = last 1%, eps = 1e-6)")
         return w, "weak"
     return w, ("weak" if (w.get("weak_support") and scaling == "weak") else "strong")
 
@@ -222,13 +222,23 @@ def build_model(w, dtype, rank, world, local):
     n = w["states"]
     sb, se = sharded.shard_ranges(n, world)[rank]
     t0 = time.time()
-    arrays = None
+    arrays = None  # this rank's host CSC arrays (the whole model at N = 1, the shard at N > 1)
     if w["source"] == "reference":
         arrays = host_arrays(w, dtype)
         if world == 1:
             m = engine.DeviceModel.from_csc(*arrays, device=local)
         else:
-            m = engine.DeviceModel.from_csc_shard(*sharded.slice_csc(*arrays, sb, se), sb, n, device=local)
+            arrays = sharded.slice_csc(*arrays, sb, se)
+            m = engine.DeviceModel.from_csc_shard(*arrays, sb, n, device=local)
+    elif w.get("host_arrays"):
+        # the counter generator on the host for this rank's states only, uploaded like a caller's arrays
+        # (so the end-to-end number includes the host -> device copy of the store)
+        arrays = engine.generate_host(gen_cfg(w, dtype, state_begin=sb if world > 1 else 0,
+                                              state_end=se if world > 1 else 0))
+        if world == 1:
+            m = engine.DeviceModel.from_csc(*arrays, device=local)
+        else:
+            m = engine.DeviceModel.from_csc_shard(*arrays, sb, n, device=local)
     else:
         cfg = gen_cfg(w, dtype, device=local, state_begin=sb if world > 1 else 0, state_end=se if world > 1 else 0)
         m = engine.DeviceModel.generate(cfg)
@@ -376,9 +386,8 @@ def engine_arm(args, w):
         log(f"[bench] e2e: model upload {1e3 * (t_up - t):.1f} ms, solve {1e3 * (time.perf_counter() - t_up):.1f} ms")
     else:
         if arrays is not None:
-            parts = sharded.slice_csc(*arrays, *sharded.shard_ranges(n, world)[rank])
-            dm = engine.DeviceModel.from_csc_shard(*parts, sharded.shard_ranges(n, world)[rank][0], n, device=local)
-            h2d += sum(a.nbytes for a in parts)
+            dm = engine.DeviceModel.from_csc_shard(*arrays, sharded.shard_ranges(n, world)[rank][0], n, device=local)
+            h2d += sum(a.nbytes for a in arrays)
         else:
             dm = m
         sh = (sharded.PeerShard if args.exchange == "peer" else sharded.NcclShard)(dm, rank, world, n) \
@@ -420,8 +429,9 @@ def engine_arm(args, w):
         "scaling": args.scaling_kind,
         "vs_baseline": None,
         "dtype": args.dtype,
-        "data": data_desc(w) + ("; generated on host, resident in HBM" if w["source"] == "reference" else
-                                "; generated directly in HBM"),
+        "data": data_desc(w) + ("; generated on host and uploaded, resident in HBM"
+                                if w["source"] == "reference" or w.get("host_arrays") else
+                                "; generated directly in HBM (the e2e number excludes the store's upload)"),
         "config": config_for(w, total_nnz, es, (f"state-sharded x{world}, V exchanged by "
                                                 + ("fused peer stores (CUDA IPC, NVLink)" if args.exchange == "peer"
                                                    else "NCCL all-gather")) if world > 1 else "single GPU"),
