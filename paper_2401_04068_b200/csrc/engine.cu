@@ -214,6 +214,12 @@ struct rimdp_model {
     cudaStream_t ls = nullptr;                // stream the next class launch goes to
     size_t l2_persist = 0;                    // bytes of L2 set aside for the value vector (0: none)
     bool pdl_now = false;                     // launches of the current iteration use PDL (launch_iteration)
+    bool gate_needed = false;                 // early class kernels: a plain launch must open the column phase
+    bool early_now = false;                   // the current iteration's class kernels start early (class_early)
+    // PDL for kernels that wait for their predecessor's output (selection / exact_dot / fallback passes,
+    // action_reduce): not behind an early-starting class kernel, whose immediate trigger would let their
+    // blocks sit resident at griddepcontrol.wait and take the running class kernel's SMs
+    bool pdl_wait_ok() const { return pdl_now && !early_now; }
     DevBuf xs_gap, xs_pos, xs_val;            // exact_sort -> exact_dot scratch (float32 exact route), by store offset
     DevBuf vrange;                            // value_range slots [2][min, max] (order keys), for omax_bucket
     int vrange_parity = 0;
@@ -778,6 +784,22 @@ void set_value_window(rimdp_model* m, const void* v, size_t bytes) {
 // ---------------------------------------------------------------------------
 // Solve loop
 
+int kernels_per_iteration(const rimdp_model* m);
+constexpr int kPdlMaxKernels = 3;
+
+// Iterations of many class kernels launch them with PDL and early start (pdl_enter_class).  Measured on C5:
+// float32 (exact route) 3.74 -> 3.66 ms, float64 2.38 -> 2.90 ms (the co-resident bucket kernels slow each
+// other down), so it is the float32 default only.  RIMDP_CLASS_EARLY=0 / 1 forces it off / on.
+bool class_early(const rimdp_model* m) {
+    static const int forced = [] {
+        const char* e = getenv("RIMDP_CLASS_EARLY");
+        return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+    }();
+    const bool want = forced >= 0 ? forced == 1 : m->dtype == RIMDP_F32;
+    return want && pdl_enabled() && kernels_per_iteration(m) > kPdlMaxKernels && !m->l2_persist &&
+           m->nstreams == 1 && m->nbatch == 0 && !(m->x.connected && m->x.shared_device);
+}
+
 template <class T>
 void upload_plan(rimdp_model* m, const rimdp_plan* p) {
     SolveState& s = m->s;
@@ -841,6 +863,7 @@ void upload_plan(rimdp_model* m, const rimdp_plan* p) {
                                cudaMemcpyHostToDevice, m->stream));
     }
     Ctl c{};
+    c.class_early = class_early(m) ? 1 : 0;
     CK(cudaMemcpyAsync(s.ctl.p, &c, sizeof c, cudaMemcpyHostToDevice, m->stream));
     s.work.ensure(2 * kWorkKinds * sizeof(unsigned));
     CK(cudaMemsetAsync(s.work.p, 0, 2 * kWorkKinds * sizeof(unsigned), m->stream));
@@ -864,7 +887,7 @@ void launch_sorted_class(rimdp_model* m, int count, const DevBuf& list, const T*
         configured[dev] = true;
     }
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
-    launch_pdl(m->pdl_now, k, blocks, Sh::threads, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
+    launch_pdl(m->pdl_wait_ok(), k, blocks, Sh::threads, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
                                                 m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, (const Ctl*)ctl,
                                                 (const int*)nullptr);
 }
@@ -885,7 +908,7 @@ void launch_select_class(rimdp_model* m, int count, const int* list, const T* V,
         configured[dev] = true;
     }
     const int blocks = grid_for(count, Sh::Groups, m->sm_count, per_sm[dev]);
-    launch_pdl(m->pdl_now, k, blocks, Sh::Block, smem, m->ls, count, list, m->colptr.as<long long>(), m->rows.as<int>(),
+    launch_pdl(m->pdl_wait_ok(), k, blocks, Sh::Block, smem, m->ls, count, list, m->colptr.as<long long>(), m->rows.as<int>(),
                                               m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl,
                                               count_dev);
 }
@@ -948,7 +971,7 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
             CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::template smem<float>()));
             fconf[dev] = true;
         }
-        launch_pdl(m->pdl_now, kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
+        launch_pdl(m->pdl_wait_ok(), kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
                    (const int*)f.list, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(),
                    m->gap.as<float>(), m->rem.as<float>(), V, q, (const Ctl*)ctl, (const int*)f.count);
     } else if constexpr (std::is_same<T, float>::value) {
@@ -976,7 +999,7 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
                    list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(), m->gap.as<float>(), V,
                    m->xs_gap.as<float>(), m->xs_pos.as<unsigned short>(), m->xs_val.as<float>(), f.list, f.count,
                    f.other, (const Ctl*)ctl);
-        launch_pdl(m->pdl_now, exact_dot, grid_for(count, kExactDotWarps, m->sm_count, dot_per_sm[dev]),
+        launch_pdl(m->pdl_wait_ok(), exact_dot, grid_for(count, kExactDotWarps, m->sm_count, dot_per_sm[dev]),
                    kExactDotWarps * 32, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
                    m->lower.as<float>(), m->rem.as<float>(), m->xs_gap.as<float>(),
                    (const unsigned short*)m->xs_pos.as<unsigned short>(), (const float*)m->xs_val.as<float>(), q,
@@ -989,7 +1012,7 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
             CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::template smem<float>()));
             fconf[dev] = true;
         }
-        launch_pdl(m->pdl_now, kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
+        launch_pdl(m->pdl_wait_ok(), kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
                    (const int*)f.list, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(),
                    m->gap.as<float>(), m->rem.as<float>(), V, q, (const Ctl*)ctl, (const int*)f.count);
     } else {
@@ -1247,6 +1270,11 @@ void launch_value_range(rimdp_model* m, const ColumnLists& L, const T* V) {
 template <class T>
 void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
     launch_value_range<T>(m, L, V);
+    if (m->gate_needed && !m->vrange_cur) { // value_range (plain launch) is the gate when it runs
+        pdl_gate<<<1, 32, 0, m->stream>>>();
+        ++g_launches;
+    }
+    m->gate_needed = false;
     ClassFanout f(m, column_classes(L));
     if (f.on) {
         if (pess)
@@ -1279,8 +1307,6 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
 // One Bellman iteration: [q path for long states: column kernels] ->
 // [fused bellman_short over the short-state batches] -> [action_reduce over
 // the long states].  The last launch of the three runs the stop test.
-int kernels_per_iteration(const rimdp_model* m);
-constexpr int kPdlMaxKernels = 3;
 
 template <class T>
 void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
@@ -1321,8 +1347,12 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     const T* rw = s.has_rewards ? s.rewards.as<T>() : nullptr;
     // PDL lets the next kernel's blocks become resident early; with two shards on one device (tests) those
     // blocks could take the SMs the other shard needs to publish the flag this shard waits for
-    m->pdl_now = kernels_per_iteration(m) <= kPdlMaxKernels && !m->l2_persist && m->nstreams == 1 &&
-                 !(m->x.connected && m->x.shared_device);
+    const bool early = class_early(m);
+    m->pdl_now = (kernels_per_iteration(m) <= kPdlMaxKernels && !m->l2_persist && m->nstreams == 1 &&
+                  !(m->x.connected && m->x.shared_device)) ||
+                 early;
+    m->gate_needed = early; // launch_columns puts a plain-launched gate before the first class kernel
+    m->early_now = early;
     if (m->nbatch > 0) {
         a.finalize = m->nlong_states == 0;
         // occupancy variant: 4 resident blocks (64 registers) or 5 (48 registers)
@@ -1343,7 +1373,7 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
         // a shard that owns no states still runs one block: its epilogue advances ctl->k and the residual
         // slots, so the sharded stop test and the solve outputs see iteration k
         a.finalize = 1;
-        launch_pdl(m->pdl_now, action_reduce<T>, grid_for(m->nlong_states, 256, m->sm_count, 8), 256, 0, m->stream,
+        launch_pdl(m->pdl_wait_ok(), action_reduce<T>, grid_for(m->nlong_states, 256, m->sm_count, 8), 256, 0, m->stream,
             a, m->nlong_states, m->long_states.as<int>(), s.q.as<T>(), vin, vout, rw, (T)s.discount, (T)s.eps, ctl);
     }
     if (m->x.connected) {
@@ -1354,6 +1384,7 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
     }
     if (ev) CK(cudaEventRecord(ev[3], m->stream));
     m->pdl_now = false;
+    m->early_now = false;
     s.launches_last = (int)(g_launches - launches0);
     CK(cudaGetLastError());
 }

@@ -91,7 +91,7 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
            const Ctl* __restrict__ ctl) {
     using Sh = ExactShape<LG>;
     constexpr int N = Sh::N, NT = Sh::NT, E = Sh::E;
-    pdl_enter();
+    pdl_enter_class(ctl);
     // the other launch parity's fallback count is cleared even by a no-op launch after the stop: the host
     // flips the parity for every launch
     if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) *fb_other = 0;
@@ -404,7 +404,7 @@ exact_warp(int nlist, const int* __restrict__ list, const long long* __restrict_
     using Sh = ExactWarpShape<LG>;
     using N_ = Num<float>;
     constexpr int N = Sh::N, E = Sh::E, W = Sh::W;
-    pdl_enter();
+    pdl_enter_class(ctl);
     if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) *fb_other = 0; // the other parity's count (see exact_sort)
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -55,7 +55,31 @@ struct Ctl {
     unsigned int arrive_stop;       // blocks of the sharded stop test that finished
     long long k;                    // iterations completed
     double res_last;                // max residual of the last iteration, as double
+    int class_early;                // many-kernel iterations: class kernels start before their predecessor ends
 };
+
+// Start of a column-class kernel.  Normally (pdl_enter) it waits for its
+// predecessor grid, then lets its successor launch.  In iterations of many
+// class kernels (C5: a dozen) the classes are independent of each other — they
+// read V_{k-1} and write disjoint q entries — so with ctl->class_early the
+// kernel lets its successor launch at once and only thread 0 of block 0 waits
+// for the predecessor: the next class's blocks take over SMs as this one's
+// blocks retire (no drain bubble between class kernels), and a grid still
+// cannot complete before its predecessor, so the action kernel (full wait)
+// sees every class finished.  The iteration's first class kernel follows a
+// plain-launched gate (value_range or pdl_gate), which orders it after the
+// previous iteration.  Kernels that read a predecessor's output (selection /
+// exact_dot / fallback passes, action_reduce) keep the full wait.
+__device__ __forceinline__ void pdl_enter_class(const Ctl* ctl) {
+    if (ctl && ctl->class_early) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+    } else {
+        pdl_enter();
+    }
+}
+
+__global__ void pdl_gate() {}
 
 // ---------------------------------------------------------------------------
 // Model preparation: per-column remainder and feasibility (omax.hpp:64-85),
@@ -270,7 +294,7 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
            unsigned* __restrict__ work) {
     using N = Num<T>;
     using Bits = typename N::Bits;
-    pdl_enter();
+    pdl_enter_class(ctl);
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     // +2: 16-byte aligned rows for the paired loads of the row-order sums, still spread over the banks
     __shared__ __align__(16) T xs[kWarpsPerBlock][kShortBatch][kShortLen + 2];
@@ -419,7 +443,7 @@ omax_tiny(int nlist, const int* __restrict__ list, const long long* __restrict__
     using N = Num<T>;
     using Bits = typename N::Bits;
     constexpr int CPW = 32 / SEG;
-    pdl_enter();
+    pdl_enter_class(ctl);
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     const int lane = threadIdx.x & 31, sg = lane / SEG, sl = lane % SEG;
     const unsigned segmask = (SEG == 32 ? kFull : ((1u << SEG) - 1u)) << (sg * SEG);
@@ -535,7 +559,7 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
     using Bits = typename N::Bits;
     using Sh = MediumShape<E>;
     constexpr int B = Sh::B, W = Sh::W, LEN = Sh::Len;
-    pdl_enter();
+    pdl_enter_class(ctl);
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     // +2: rows stay 16-byte aligned for the vector product stores and lane t's sequential reads of row t
     // still spread over the banks
@@ -742,7 +766,7 @@ omax_long(int nlist, const int* __restrict__ list, const long long* __restrict__
     using N = Num<T>;
     using Bits = typename N::Bits;
     constexpr int K = kLongTopK, U = 4, G = kLongGroup;
-    pdl_enter();
+    pdl_enter_class(ctl);
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     constexpr int UB = 2; // phase B: chunks per round
     __shared__ T xs[kWarpsPerBlock][G][32 * UB + 1];
@@ -999,7 +1023,7 @@ omax_long_tree(int nlist, const int* __restrict__ list, const long long* __restr
     using N = Num<T>;
     using Bits = typename N::Bits;
     constexpr int K = kLongTopK, U = 4;
-    pdl_enter();
+    pdl_enter_class(ctl);
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     extern __shared__ __align__(16) unsigned char vs_raw[];
     const T* __restrict__ V = Vg;
@@ -1828,7 +1852,7 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
     using Bits = typename N::Bits;
     using Sh = BucketShape<LG, T>;
     constexpr int E = Sh::E, NT = Sh::NT, NW = Sh::NW, B = Sh::B, CAP = kBucketCap;
-    pdl_enter();
+    pdl_enter_class(ctl);
     // fallback counters alternate between launches: this launch counts into
     // nfallback and clears the other one for the next launch (every earlier
     // launch, and the selection pass that read it, has completed)
@@ -2098,7 +2122,7 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
     using Bits = typename N::Bits;
     using Sh = WBucketShape<LG>;
     constexpr int E = Sh::E, B = Sh::B, PB = Sh::PB, W = Sh::W;
-    pdl_enter();
+    pdl_enter_class(ctl);
     if (blockIdx.x == 0 && threadIdx.x == 0) *other_nfallback = 0;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     __shared__ __align__(16) unsigned char smem[W * Sh::WarpBytes];
