@@ -196,6 +196,7 @@ struct rimdp_model {
     bool all_is_qp = false;                   // every column is on the q path: `all` is `qp`
     const ColumnLists& all_lists() const { return all_is_qp ? qp : all; }
     int nbatch = 0, nlong_states = 0;         // fused short-state batches / q-path states
+    bool all_states_q = true;                 // every state on the q path, in order: no state list
     std::vector<int> h_stateptr;
     std::vector<Infeasible> infeasible_cols;
     long long device_bytes = 0;
@@ -503,6 +504,7 @@ int column_class(long long len, double rem, double maxgap, int mode) {
 void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, const std::vector<signed char>& cls,
                 const long long* by_length = nullptr) {
     std::vector<int> sh, ex, md[2], ti[3], so[kSortedClasses];
+    if (!cols.empty() && cls[cols.front()] == 0 && cls[cols.back()] == 0) sh.reserve(cols.size());
     for (int c : cols) {
         const int k = cls[c];
         if (k == 0) sh.push_back(c);
@@ -544,8 +546,12 @@ void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, co
 template <class T>
 void build_schedule(rimdp_model* m, const long long* h_colptr) {
     PhaseTrace tr("schedule");
-    std::vector<T> h_rem(m->ncols), h_maxgap(m->ncols);
-    if (m->ncols > 0) {
+    // the pick-count test (rem vs maxgap) only matters for columns longer than a warp: models without such
+    // columns (config 2) skip the device -> host copy of rem / maxgap
+    bool any_long = false;
+    for (int c = 0; c < m->ncols && !any_long; ++c) any_long = h_colptr[c + 1] - h_colptr[c] > kShortLen;
+    std::vector<T> h_rem(any_long ? m->ncols : 0), h_maxgap(any_long ? m->ncols : 0);
+    if (m->ncols > 0 && any_long) {
         CK(cudaMemcpyAsync(h_rem.data(), m->rem.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
         CK(cudaMemcpyAsync(h_maxgap.data(), m->maxgap.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
         CK(cudaStreamSynchronize(m->stream));
@@ -572,7 +578,8 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     for (int c = 0; c < m->ncols; ++c) {
         const long long len = h_colptr[c + 1] - h_colptr[c];
         maxlen = (int)std::max<long long>(maxlen, len);
-        cls[c] = (signed char)column_class(len, (double)h_rem[c], (double)h_maxgap[c], mode);
+        cls[c] = (signed char)column_class(len, any_long ? (double)h_rem[c] : 0.0,
+                                           any_long ? (double)h_maxgap[c] : 0.0, mode);
         allc[c] = c;
     }
     const std::vector<int>& sp = m->h_stateptr;
@@ -589,13 +596,16 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     std::vector<int> slots, lstates;
     std::vector<int2> bstates;
     int s0 = -1, used = 0;
+    // the default (no fused short-state batches): every state is a q-path state and every column a q-path
+    // column, in order — the action kernel then walks the states directly (no state list)
+    m->all_states_q = !fused;
     auto close_batch = [&]() {
         if (s0 < 0) return;
         for (int j = used; j < kShortBatch; ++j) slots.push_back(-1);
         s0 = -1;
         used = 0;
     };
-    for (int s = 0; s < m->n; ++s) {
+    for (int s = 0; s < m->n && fused; ++s) {
         if (!short_state(s)) {
             close_batch();
             lstates.push_back(s);
@@ -613,6 +623,7 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         bstates.back().y += 1;
     }
     close_batch();
+    if (!fused) qc = allc;
     tr.mark("classify");
     m->maxlen = maxlen;
     // every column on the q path (the default: no fused short-state batches): the two sets of lists are the
@@ -623,7 +634,7 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     fill_lists(m, m->qp, qc, cls, by_len);
     tr.mark("lists");
     m->nbatch = (int)bstates.size();
-    m->nlong_states = (int)lstates.size();
+    m->nlong_states = m->all_states_q ? m->n : (int)lstates.size();
     upload_list(m, m->batch_slots, slots);
     upload_list(m, m->batch_states, bstates);
     upload_list(m, m->long_states, lstates);
@@ -1374,7 +1385,8 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
         // slots, so the sharded stop test and the solve outputs see iteration k
         a.finalize = 1;
         launch_pdl(m->pdl_wait_ok(), action_reduce<T>, grid_for(m->nlong_states, 256, m->sm_count, 8), 256, 0, m->stream,
-            a, m->nlong_states, m->long_states.as<int>(), s.q.as<T>(), vin, vout, rw, (T)s.discount, (T)s.eps, ctl);
+            a, m->nlong_states, m->all_states_q ? nullptr : m->long_states.as<int>(), s.q.as<T>(), vin, vout, rw,
+            (T)s.discount, (T)s.eps, ctl);
     }
     if (m->x.connected) {
         // the global stop test once every rank has published iteration k (peer_sync_stop)
