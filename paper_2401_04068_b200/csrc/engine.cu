@@ -1823,8 +1823,18 @@ static int check_plan(rimdp_model* m, const rimdp_plan* p) {
     return RIMDP_OK;
 }
 
+// A shard connected to peers only iterates together with them (begin / advance / poll / finish on every
+// rank, or rimdp_multi_solve): a lone solve or step would wait forever for the peers' flags.
+static int reject_connected(rimdp_model* m, const char* what) {
+    if (m && m->x.connected && m->x.world > 1)
+        return fail(RIMDP_ERR_INVALID_ARGUMENT, "%s: this model is a connected shard of a %d-rank solve", what,
+                    m->x.world);
+    return RIMDP_OK;
+}
+
 int rimdp_solve(rimdp_model* m, const rimdp_plan* p, const rimdp_outputs* o) {
     if (int st = check_plan(m, p)) return st;
+    if (int st = reject_connected(m, "rimdp_solve")) return st;
     return guarded([&]() -> int {
         DeviceGuard g(m->device);
         rimdp_outputs none{};
@@ -2096,6 +2106,7 @@ int rimdp_bellman_step(rimdp_model* m, const void* v_in, int32_t pess, int32_t m
     p.finite = 1;
     p.horizon = 1;
     if (int st = check_plan(m, &p)) return st;
+    if (int st = reject_connected(m, "rimdp_bellman_step")) return st;
     return guarded([&]() -> int {
         DeviceGuard g(m->device);
         return DISPATCH(m, step_t, m, v_in, pess, maxi, frozen, forced, v_out, chosen_out);

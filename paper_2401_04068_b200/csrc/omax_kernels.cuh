@@ -623,11 +623,11 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
             // greedy O-max of column s (omax.hpp:98-112)
             const T r = __shfl_sync(kFull, mrem, s);
             Bits key[E];
-            T p[E];
+            T pick_avail[E]; // avail at this entry's pick, -1 if not picked (picks only happen with avail > 0)
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 key[e] = j0 + e < Lc ? order_key<T>(vc[e], kPess) : ~Bits(0);
-                p[e] = lc[e];
+                pick_avail[e] = T(-1);
             }
             T consumed = T(0), avail = r;
             for (int nsel = 0; avail > T(0) && nsel < Lc; ++nsel) {
@@ -641,19 +641,33 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
                         be = e;
                     }
                 bool cand = true;
+                unsigned single = 0u; // a lane whose high key word is the unique minimum decides alone
                 if constexpr (sizeof(Bits) == 8) {
                     const unsigned hi = static_cast<unsigned>(bk >> 32), lo = static_cast<unsigned>(bk);
                     const unsigned mhi = __reduce_min_sync(kFull, hi);
                     cand = hi == mhi;
-                    const unsigned mlo = __reduce_min_sync(kFull, cand ? lo : 0xffffffffu);
-                    cand = cand && lo == mlo;
+                    const unsigned wh = __ballot_sync(kFull, cand);
+                    if ((wh & (wh - 1u)) == 0u) {
+                        single = wh;
+                    } else {
+                        const unsigned mlo = __reduce_min_sync(kFull, cand ? lo : 0xffffffffu);
+                        cand = cand && lo == mlo;
+                    }
                 } else {
                     const unsigned mk = __reduce_min_sync(kFull, static_cast<unsigned>(bk));
                     cand = static_cast<unsigned>(bk) == mk;
                 }
-                // ties of the key go to the lowest position = row (csc.hpp:98-101)
-                const unsigned pos = __reduce_min_sync(kFull, cand ? static_cast<unsigned>(j0 + be) : 0xffffffffu);
-                const int sel_lane = static_cast<int>(pos / E), sel_e = static_cast<int>(pos % E);
+                // ties of the key go to the lowest position = row (csc.hpp:98-101); a lane's own entries are
+                // in position order, so its (key, e) minimum already prefers the lower e on ties
+                int sel_lane, sel_e;
+                if (single) {
+                    sel_lane = __ffs(single) - 1;
+                    sel_e = __shfl_sync(kFull, be, sel_lane);
+                } else {
+                    const unsigned pos = __reduce_min_sync(kFull, cand ? static_cast<unsigned>(j0 + be) : 0xffffffffu);
+                    sel_lane = static_cast<int>(pos / E);
+                    sel_e = static_cast<int>(pos % E);
+                }
                 T mine = gc[0];
 #pragma unroll
                 for (int e = 1; e < E; ++e)
@@ -663,7 +677,7 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
 #pragma unroll
                     for (int e = 0; e < E; ++e)
                         if (e == sel_e) {
-                            p[e] = N::add(lc[e], gc[e] < avail ? gc[e] : avail);
+                            pick_avail[e] = avail;
                             key[e] = ~Bits(0);
                         }
                 }
@@ -673,7 +687,11 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
             {
                 T x[E];
 #pragma unroll
-                for (int e = 0; e < E; ++e) x[e] = N::mul(vc[e], p[e]); // entries past the column are never read
+                for (int e = 0; e < E; ++e) { // omax.hpp:107; entries past the column are never read
+                    const T a = pick_avail[e];
+                    const T p = a > T(0) ? N::add(lc[e], gc[e] < a ? gc[e] : a) : lc[e];
+                    x[e] = N::mul(vc[e], p);
+                }
                 if constexpr (E == 2 && sizeof(T) == 8) {
                     *reinterpret_cast<double2*>(&xs[w][s][j0]) = make_double2(x[0], x[1]);
                 } else {
@@ -698,7 +716,16 @@ omax_medium(int nlist, const int* __restrict__ list, const long long* __restrict
         __syncwarp();
         if (lane < B && mc >= 0) {
             T acc = T(0);
-            for (int i = 0; i < mlen; ++i) acc = N::add(acc, xs[w][lane][i]);
+            int i = 0;
+            if constexpr (sizeof(T) == 8) {
+                const double2* x2 = reinterpret_cast<const double2*>(xs[w][lane]);
+                for (; i + 2 <= mlen; i += 2) {
+                    const double2 y = x2[i >> 1];
+                    acc = N::add(acc, y.x);
+                    acc = N::add(acc, y.y);
+                }
+            }
+            for (; i < mlen; ++i) acc = N::add(acc, xs[w][lane][i]);
             q[mc] = acc;
         }
         __syncwarp();

@@ -186,3 +186,25 @@ def test_one_rank_nccl_baseline_matches_engine_solve():
             assert np.array_equal(bits(out.residual), bits(ref["residual"]))
     finally:
         dist.destroy_process_group()
+
+
+def test_connected_shard_refuses_lone_solves():
+    """A shard connected to peers iterates only together with them: a lone rimdp_solve / bellman_step is
+    refused (it would wait forever for the peers' flags); column values need no exchange and still work."""
+    arrays = csc_model()
+    n = len(arrays[0]) - 1
+    parts = [engine.DeviceModel.from_csc_shard(*sharded.slice_csc(*arrays, sb, se), sb, n)
+             for sb, se in sharded.shard_ranges(n, 2)]
+    for p in parts:
+        p.set_value_capacity(n)
+    engine.connect_local(parts)
+    goal = np.zeros(n, np.uint8)
+    goal[-10:] = 1
+    for call in (lambda: parts[0].solve(initial=goal.astype(np.float64), frozen=goal, finite=True, horizon=3),
+                 lambda: parts[1].bellman_step(goal.astype(np.float64))):
+        with pytest.raises(engine.EngineError) as e:
+            call()
+        assert e.value.status == engine.ERR_INVALID_ARGUMENT and "connected shard" in e.value.message
+    q = parts[0].column_values(np.random.default_rng(1).random(n))
+    ref = engine.DeviceModel.from_csc(*arrays).column_values(np.random.default_rng(1).random(n))
+    assert np.array_equal(bits(q), bits(ref[:len(q)]))
