@@ -456,6 +456,15 @@ void upload_list(rimdp_model* m, DevBuf& buf, const std::vector<U>& v) {
 // Routing mode for long columns (tests): RIMDP_LONG=exact (every long column
 // on the exact warp kernel), sorted (every one on the bitonic CTA kernel),
 // select (every one on the selection kernels, no value buckets).
+// 17-32-entry columns: two per warp step (omax_pair) by default; RIMDP_PAIR=0 -> one per step (omax_short)
+bool pair_mode() {
+    static const bool on = [] {
+        const char* e = getenv("RIMDP_PAIR");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 bool env_flag(const char* name) {
     const char* e = getenv(name);
     return e && atoi(e) != 0;
@@ -1295,8 +1304,10 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
     }
     if (L.n_short > 0) {
         f.pick();
-        const int blocks = grid_for(L.n_short, kShortBatch * kWarpsPerBlock, m->sm_count, 5);
-        auto k = pess ? omax_short<T, true> : omax_short<T, false>;
+        const bool pair = pair_mode();
+        const int blocks = grid_for(L.n_short, kShortBatch * kWarpsPerBlock, m->sm_count, pair ? 4 : 5);
+        auto k = pair ? (pess ? omax_pair<T, true> : omax_pair<T, false>)
+                      : (pess ? omax_short<T, true> : omax_short<T, false>);
         launch_pdl(m->pdl_now, k, blocks, kWarpsPerBlock * 32, 0, m->ls, L.n_short, L.short_list.as<int>(), m->colptr.as<long long>(),
                                                       m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(),
                                                       m->rem.as<T>(), V, q, ctl, work);

@@ -426,6 +426,210 @@ omax_short(int nlist, const int* __restrict__ list, const long long* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// Short columns (17 .. 32 entries), two per warp step (omax_pair): lanes
+// 0-15 take column A, lanes 16-31 column B, lane l of a half owning the two
+// consecutive entries 2l, 2l+1 — one 128-bit load per array (`double2`
+// lower / gap, `int2` rows) when the column starts on an even entry.  The two
+// greedy loops (omax.hpp:98-112) run side by side: each pick step is one
+// half-masked exact argmin per column over (order key, position) and one
+// shuffle of the winners' gaps, so the per-pick and per-column instructions
+// (reductions, metadata shuffles, loop control) serve two columns.  Products
+// are staged in shared memory and lane t sums column t in row order
+// (omax.hpp:169-173), as in omax_short: bit-exact.  Same three-deep
+// pipeline as omax_short, one pair per stage.
+template <class T, bool kPess>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
+omax_pair(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+          const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+          const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl,
+          unsigned* __restrict__ work) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    constexpr int P = kShortBatch / 2; // pairs per batch
+    pdl_enter_class(ctl);
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    __shared__ __align__(16) T xs[kWarpsPerBlock][kShortBatch][kShortLen + 2];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int h = lane >> 4, j0 = 2 * (lane & 15);
+    const unsigned half = h ? 0xffff0000u : 0x0000ffffu;
+    const unsigned long long pstream = l2_evict_first_policy();
+    const int gw = blockIdx.x * kWarpsPerBlock + w, nw = gridDim.x * kWarpsPerBlock;
+    auto next_batch = [&]() -> int {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(work, 1u);
+        return nw + static_cast<int>(__shfl_sync(kFull, t, 0));
+    };
+    int base = gw * kShortBatch;
+    if (base >= nlist) return;
+    int nbase = next_batch() * kShortBatch;
+
+    // metadata window: lane j describes column j of [current batch | next batch]
+    int mc = -1, mlen = 0;
+    long long mbeg = 0;
+    T mrem = T(0);
+    auto load_meta = [&](int batch_base) {
+        const int idx = batch_base + (lane & (kShortBatch - 1));
+        mc = -1;
+        mlen = 0;
+        mbeg = 0;
+        mrem = T(0);
+        if (batch_base < nlist && idx < nlist) {
+            mc = __ldg(list + idx);
+            mbeg = __ldg(colptr + mc);
+            mlen = static_cast<int>(__ldg(colptr + mc + 1) - mbeg);
+            mrem = __ldg(rem + mc);
+        }
+    };
+    load_meta(lane < kShortBatch ? base : nbase);
+    auto gather = [&](const int (&rw)[2], int L, T (&v)[2]) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) v[e] = j0 + e < L ? __ldg(V + rw[e]) : T(0);
+    };
+
+    // pipeline prologue: data of pair 0, rows of pair 1 (this lane's column of each)
+    long long bn = __shfl_sync(kFull, mbeg, h), bnn = __shfl_sync(kFull, mbeg, 2 + h);
+    int Ln = __shfl_sync(kFull, mlen, h), Lnn = __shfl_sync(kFull, mlen, 2 + h);
+    int rowA[2], rowB[2];
+    T lc[2], gc[2], vc[2], ln[2], gn[2], vn[2];
+    ld_run<2>(rows + bn, j0, Ln, (bn & 1) == 0, pstream, rowA);
+    ld_run<2>(lower + bn, j0, Ln, (bn & 1) == 0, pstream, lc);
+    ld_run<2>(gap + bn, j0, Ln, (bn & 1) == 0, pstream, gc);
+    gather(rowA, Ln, vc);
+    int Lc = Ln;
+    bn = bnn;
+    Ln = Lnn;
+    ld_run<2>(rows + bn, j0, Ln, (bn & 1) == 0, pstream, rowA);
+    bnn = __shfl_sync(kFull, mbeg, 4 + h);
+    Lnn = __shfl_sync(kFull, mlen, 4 + h);
+
+    for (;;) {
+        for (int s = 0; s < P; ++s) {
+            // stage D: (lower, gap, V[row]) of pair i+1; stage R: rows of pair i+2
+            ld_run<2>(lower + bn, j0, Ln, (bn & 1) == 0, pstream, ln);
+            ld_run<2>(gap + bn, j0, Ln, (bn & 1) == 0, pstream, gn);
+            gather(rowA, Ln, vn);
+            ld_run<2>(rows + bnn, j0, Lnn, (bnn & 1) == 0, pstream, rowB);
+            // stage C: the two greedy O-maxes of pair i
+            const T r = __shfl_sync(kFull, mrem, 2 * s + h);
+            Bits key[2];
+            T pa[2]; // avail at this entry's pick, -1 if not picked (picks only happen with avail > 0)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                key[e] = j0 + e < Lc ? order_key<T>(vc[e], kPess) : ~Bits(0);
+                pa[e] = T(-1);
+            }
+            T consumed = T(0), avail = r;
+            for (int nsel = 0;; ++nsel) {
+                const bool act = avail > T(0) && nsel < Lc;
+                if (!__any_sync(kFull, act)) break;
+                const bool second = key[1] < key[0]; // ties keep the lower position
+                const Bits bk = second ? key[1] : key[0];
+                bool cand;
+                unsigned wb;
+                if constexpr (sizeof(Bits) == 8) {
+                    const unsigned hi = act ? static_cast<unsigned>(bk >> 32) : 0xffffffffu;
+                    const unsigned m0 = __reduce_min_sync(kFull, h == 0 ? hi : 0xffffffffu);
+                    const unsigned m1 = __reduce_min_sync(kFull, h == 1 ? hi : 0xffffffffu);
+                    cand = act && hi == (h ? m1 : m0);
+                    wb = __ballot_sync(kFull, cand);
+                    const unsigned a = wb & 0xffffu, b = wb >> 16;
+                    if ((a & (a - 1u)) | (b & (b - 1u))) { // a half with several equal high words
+                        const unsigned lo = cand ? static_cast<unsigned>(bk) : 0xffffffffu;
+                        const unsigned l0 = __reduce_min_sync(kFull, h == 0 ? lo : 0xffffffffu);
+                        const unsigned l1 = __reduce_min_sync(kFull, h == 1 ? lo : 0xffffffffu);
+                        cand = cand && lo == (h ? l1 : l0);
+                        wb = __ballot_sync(kFull, cand);
+                    }
+                } else {
+                    const unsigned k = act ? static_cast<unsigned>(bk) : 0xffffffffu;
+                    const unsigned m0 = __reduce_min_sync(kFull, h == 0 ? k : 0xffffffffu);
+                    const unsigned m1 = __reduce_min_sync(kFull, h == 1 ? k : 0xffffffffu);
+                    cand = act && k == (h ? m1 : m0);
+                    wb = __ballot_sync(kFull, cand);
+                }
+                // lowest lane of the half among equal keys = lowest position (rows ascending, csc.hpp:98-101)
+                const unsigned mine = wb & half;
+                const int sel = mine ? __ffs(mine) - 1 : lane;
+                const T gs = __shfl_sync(kFull, second ? gc[1] : gc[0], sel);
+                if (act) {
+                    if (lane == sel) {
+                        if (second) {
+                            pa[1] = avail;
+                            key[1] = ~Bits(0);
+                        } else {
+                            pa[0] = avail;
+                            key[0] = ~Bits(0);
+                        }
+                    }
+                    consumed = N::add(consumed, gs);
+                    avail = N::sub(r, consumed);
+                }
+            }
+            {   // omax.hpp:107: p = lower + (gap < avail ? gap : avail) for a picked position, lower otherwise
+                T x[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const T p = pa[e] > T(0) ? N::add(lc[e], gc[e] < pa[e] ? gc[e] : pa[e]) : lc[e];
+                    x[e] = N::mul(vc[e], p);
+                }
+                if constexpr (sizeof(T) == 8) {
+                    *reinterpret_cast<double2*>(&xs[w][2 * s + h][j0]) = make_double2(x[0], x[1]);
+                } else {
+                    xs[w][2 * s + h][j0] = x[0];
+                    xs[w][2 * s + h][j0 + 1] = x[1];
+                }
+            }
+            // rotate the pipeline; metadata of pair i+3 = window lanes 2(s+3), 2(s+3)+1
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                lc[e] = ln[e];
+                gc[e] = gn[e];
+                vc[e] = vn[e];
+                rowA[e] = rowB[e];
+            }
+            Lc = Ln;
+            bn = bnn;
+            Ln = Lnn;
+            bnn = __shfl_sync(kFull, mbeg, (2 * (s + 3) + h) & 31);
+            Lnn = __shfl_sync(kFull, mlen, (2 * (s + 3) + h) & 31);
+        }
+        // row-order expectation of the batch's columns (omax.hpp:169-173)
+        __syncwarp();
+        if (lane < kShortBatch && mc >= 0) {
+            T acc = T(0);
+            int i = 0;
+            if constexpr (sizeof(T) == 8) {
+                const double2* x2 = reinterpret_cast<const double2*>(xs[w][lane]);
+                for (; i + 2 <= mlen; i += 2) {
+                    const double2 y = x2[i >> 1];
+                    acc = N::add(acc, y.x);
+                    acc = N::add(acc, y.y);
+                }
+            }
+            for (; i < mlen; ++i) acc = N::add(acc, xs[w][lane][i]);
+            q[mc] = acc;
+        }
+        __syncwarp();
+        base = nbase;
+        if (base >= nlist) break;
+        nbase = next_batch() * kShortBatch;
+        // shift the window and prefetch the batch after next
+        const int c2 = __shfl_down_sync(kFull, mc, kShortBatch);
+        const long long b2 = __shfl_down_sync(kFull, mbeg, kShortBatch);
+        const int l2 = __shfl_down_sync(kFull, mlen, kShortBatch);
+        const T r2 = __shfl_down_sync(kFull, mrem, kShortBatch);
+        if (lane < kShortBatch) {
+            mc = c2;
+            mbeg = b2;
+            mlen = l2;
+            mrem = r2;
+        } else {
+            load_meta(nbase);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Tiny columns (<= SEG entries, SEG = 4, 8 or 16): 32 / SEG columns per warp
 // step, one SEG-lane segment per column (power-law models are dominated by
 // columns of 1-4 entries, which would leave most of omax_short's lanes
