@@ -197,6 +197,7 @@ struct rimdp_model {
     const ColumnLists& all_lists() const { return all_is_qp ? qp : all; }
     int nbatch = 0, nlong_states = 0;         // fused short-state batches / q-path states
     bool all_states_q = true;                 // every state on the q path, in order: no state list
+    bool short_pair = true;                   // 17-32-entry class on omax_pair (nearly full columns)
     std::vector<int> h_stateptr;
     std::vector<Infeasible> infeasible_cols;
     long long device_bytes = 0;
@@ -635,6 +636,17 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     if (!fused) qc = allc;
     tr.mark("classify");
     m->maxlen = maxlen;
+    {   // omax_pair pays off when the two columns of a step are nearly full (config 2: all 32 entries); with
+        // the mixed 17-32 lengths of a power-law model (mean ~24) the pair's loop runs the longer column's
+        // picks for both and measured 2% slower than omax_short
+        long long cnt = 0, tot = 0;
+        for (int c = 0; c < m->ncols; ++c)
+            if (cls[c] == 0) {
+                ++cnt;
+                tot += h_colptr[c + 1] - h_colptr[c];
+            }
+        m->short_pair = cnt == 0 || tot >= 28 * cnt;
+    }
     // every column on the q path (the default: no fused short-state batches): the two sets of lists are the
     // same, so `all` is not built separately
     m->all_is_qp = qc.size() == allc.size();
@@ -1304,7 +1316,7 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
     }
     if (L.n_short > 0) {
         f.pick();
-        const bool pair = pair_mode();
+        const bool pair = pair_mode() && m->short_pair;
         const int blocks = grid_for(L.n_short, kShortBatch * kWarpsPerBlock, m->sm_count, pair ? 4 : 5);
         auto k = pair ? (pess ? omax_pair<T, true> : omax_pair<T, false>)
                       : (pess ? omax_short<T, true> : omax_short<T, false>);
