@@ -138,6 +138,10 @@ constexpr double kExactPickBudget = 4.0;
 struct ColumnLists {
     DevBuf short_list, exact_list, medium_list[2], tiny_list[3], sorted_list[kSortedClasses];
     int n_short = 0, n_exact = 0, n_medium[2] = {}, n_tiny[3] = {}, n_sorted[kSortedClasses] = {};
+    // tiny classes packed in list order (pack_columns): begins [n + 1], rem [n], rows / lower / gap
+    DevBuf tiny_beg[3], tiny_rem[3], tiny_rows[3], tiny_lower[3], tiny_gap[3];
+    bool tiny_packed[3] = {};
+    std::vector<int> tiny_host[3]; // the lists on the host, until packed
     int total_sorted() const {
         int t = 0;
         for (int i = 0; i < kSortedClasses; ++i) t += n_sorted[i];
@@ -201,6 +205,7 @@ struct rimdp_model {
     std::vector<int> h_stateptr;
     std::vector<Infeasible> infeasible_cols;
     long long device_bytes = 0;
+    long long pack_bytes = 0; // the packed tiny classes (pack_tiny)
     int sm_count = 148;
     int short_blocks_per_sm = 4;
     bool bitonic = false;                     // many-pick long columns: bitonic sort instead of selection
@@ -534,6 +539,7 @@ void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, co
     for (int i = 0; i < 3; ++i) {
         L.n_tiny[i] = (int)ti[i].size();
         upload_list(m, L.tiny_list[i], ti[i]);
+        L.tiny_host[i] = std::move(ti[i]);
     }
     for (int i = 0; i < kSortedClasses; ++i) {
         if (by_length)
@@ -553,9 +559,59 @@ void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, co
 //    (<= 16 columns, all columns <= 32 entries) are packed into state-aligned
 //    batches of <= 16 column slots for the fused bellman_short kernel; the
 //    remaining states take the q path (column kernels + action_reduce).
+// Tiny classes of power-law models are packed in list order at upload (pack_tiny): the kernels then stream
+// contiguous runs.  RIMDP_TINY_PACK=0 keeps them reading the store in place.
+bool tiny_pack_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("RIMDP_TINY_PACK");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+template <class T>
+void pack_tiny(rimdp_model* m, ColumnLists& L, const long long* h_colptr) {
+    for (int i = 0; i < 3; ++i) {
+        std::vector<int>& lst = L.tiny_host[i];
+        L.tiny_packed[i] = false;
+        if (lst.empty() || !tiny_pack_enabled()) {
+            lst.clear();
+            continue;
+        }
+        const int n = (int)lst.size();
+        std::vector<long long> beg(n + 1, 0);
+        for (int k = 0; k < n; ++k) beg[k + 1] = beg[k] + (h_colptr[lst[k] + 1] - h_colptr[lst[k]]);
+        const size_t z = (size_t)std::max<long long>(beg[n], 1);
+        const size_t need = sizeof(long long) * (n + 1) + sizeof(T) * n + (sizeof(int) + 2 * sizeof(T)) * z;
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        if (need + (size_t(2) << 30) > free_b) { // a copy is an optimisation: never trade the headroom for it
+            lst.clear();
+            continue;
+        }
+        L.tiny_beg[i].ensure(sizeof(long long) * (n + 1));
+        L.tiny_rem[i].ensure(sizeof(T) * n);
+        L.tiny_rows[i].ensure(sizeof(int) * z);
+        L.tiny_lower[i].ensure(sizeof(T) * z);
+        L.tiny_gap[i].ensure(sizeof(T) * z);
+        CK(cudaMemcpyAsync(L.tiny_beg[i].p, beg.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, m->stream));
+        pack_columns<T><<<grid_for(n, 256, m->sm_count, 8), 256, 0, m->stream>>>(
+            n, L.tiny_list[i].as<int>(), m->colptr.as<long long>(), L.tiny_beg[i].as<long long>(), m->rows.as<int>(),
+            m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), L.tiny_rows[i].as<int>(), L.tiny_lower[i].as<T>(),
+            L.tiny_gap[i].as<T>(), L.tiny_rem[i].as<T>());
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(m->stream)); // `beg` is a host temporary
+        L.tiny_packed[i] = true;
+        m->pack_bytes += (long long)need;
+        lst.clear();
+        lst.shrink_to_fit();
+    }
+}
+
 template <class T>
 void build_schedule(rimdp_model* m, const long long* h_colptr) {
     PhaseTrace tr("schedule");
+    m->pack_bytes = 0;
     // the pick-count test (rem vs maxgap) only matters for columns longer than a warp: models without such
     // columns (config 2) skip the device -> host copy of rem / maxgap
     bool any_long = false;
@@ -653,6 +709,8 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     const long long* by_len = m->exact_sorted ? h_colptr : nullptr;
     if (!m->all_is_qp) fill_lists(m, m->all, allc, cls, by_len);
     fill_lists(m, m->qp, qc, cls, by_len);
+    if (!m->all_is_qp) pack_tiny<T>(m, m->all, h_colptr);
+    pack_tiny<T>(m, m->qp, h_colptr);
     tr.mark("lists");
     m->nbatch = (int)bstates.size();
     m->nlong_states = m->all_states_q ? m->n : (int)lstates.size();
@@ -1137,8 +1195,11 @@ void launch_medium(rimdp_model* m, int count, const DevBuf& list, const T* V, T*
 }
 
 template <class T, int SEG>
-void launch_tiny(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl, bool pess) {
-    auto k = pess ? omax_tiny<T, true, SEG> : omax_tiny<T, false, SEG>;
+void launch_tiny(rimdp_model* m, const ColumnLists& L, int i, const T* V, T* q, Ctl* ctl, bool pess) {
+    const int count = L.n_tiny[i];
+    const bool pk = L.tiny_packed[i];
+    auto k = pk ? (pess ? omax_tiny<T, true, SEG, true> : omax_tiny<T, false, SEG, true>)
+                : (pess ? omax_tiny<T, true, SEG> : omax_tiny<T, false, SEG>);
     static int per_sm[64] = {};
     const int dev = m->device & 63;
     if (!per_sm[dev]) {
@@ -1147,8 +1208,13 @@ void launch_tiny(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q
     }
     const int steps = (count + 32 / SEG - 1) / (32 / SEG);
     const int blocks = grid_for(steps, 8 * 4, m->sm_count, per_sm[dev]); // >= 4 steps per warp
-    launch_pdl(m->pdl_now, k, blocks, 256, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(),
-                                      m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
+    if (pk)
+        launch_pdl(m->pdl_now, k, blocks, 256, 0, m->ls, count, L.tiny_list[i].as<int>(), L.tiny_beg[i].as<long long>(),
+                   L.tiny_rows[i].as<int>(), L.tiny_lower[i].as<T>(), L.tiny_gap[i].as<T>(), L.tiny_rem[i].as<T>(), V,
+                   q, ctl);
+    else
+        launch_pdl(m->pdl_now, k, blocks, 256, 0, m->ls, count, L.tiny_list[i].as<int>(), m->colptr.as<long long>(),
+                   m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl);
 }
 
 template <class T, bool P, bool VS>
@@ -1327,9 +1393,9 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
     if (L.n_medium[0] > 0) { f.pick(); launch_medium<T, 2>(m, L.n_medium[0], L.medium_list[0], V, q, ctl, pess, work + 2); }
     if (L.n_medium[1] > 0) { f.pick(); launch_medium<T, 4>(m, L.n_medium[1], L.medium_list[1], V, q, ctl, pess, work + 3); }
     if (L.n_exact > 0) { f.pick(); launch_long<T>(m, L.n_exact, L.exact_list, V, q, ctl, pess); }
-    if (L.n_tiny[2] > 0) { f.pick(); launch_tiny<T, 16>(m, L.n_tiny[2], L.tiny_list[2], V, q, ctl, pess); }
-    if (L.n_tiny[1] > 0) { f.pick(); launch_tiny<T, 8>(m, L.n_tiny[1], L.tiny_list[1], V, q, ctl, pess); }
-    if (L.n_tiny[0] > 0) { f.pick(); launch_tiny<T, 4>(m, L.n_tiny[0], L.tiny_list[0], V, q, ctl, pess); }
+    if (L.n_tiny[2] > 0) { f.pick(); launch_tiny<T, 16>(m, L, 2, V, q, ctl, pess); }
+    if (L.n_tiny[1] > 0) { f.pick(); launch_tiny<T, 8>(m, L, 1, V, q, ctl, pess); }
+    if (L.n_tiny[0] > 0) { f.pick(); launch_tiny<T, 4>(m, L, 0, V, q, ctl, pess); }
     if (!f.on) {
         if (pess)
             launch_sorted<T, true>(m, L, V, q, ctl);
@@ -1775,7 +1841,7 @@ static int model_create_impl(const rimdp_model_desc* d, int state_begin, int num
         tr.mark("schedule");
         m->device_bytes = (long long)(m->stateptr.bytes + m->colptr.bytes + m->rows.bytes + m->lower.bytes +
                                       m->gap.bytes + m->rem.bytes + m->infeasible.bytes + m->quoted.bytes +
-                                      m->maxgap.bytes);
+                                      m->maxgap.bytes + m->pack_bytes);
         *out = m.release();
         return RIMDP_OK;
     });
@@ -2257,7 +2323,7 @@ void generate_t(rimdp_model* m, const GenSetup& g) {
     build_schedule<T>(m, h_colptr.data());
     m->device_bytes = (long long)(m->stateptr.bytes + m->colptr.bytes + m->rows.bytes + m->lower.bytes +
                                   m->gap.bytes + m->rem.bytes + m->infeasible.bytes + m->quoted.bytes +
-                                  m->maxgap.bytes);
+                                  m->maxgap.bytes + m->pack_bytes);
 }
 
 template <class T>

@@ -639,7 +639,13 @@ omax_pair(int nlist, const int* __restrict__ list, const long long* __restrict__
 // segment's products to its first lane (omax.hpp:169-173): bit-exact.
 // Two-stage pipeline: the next step's metadata and rows are in flight while
 // the current step is reduced.
-template <class T, bool kPess, int SEG>
+// kPacked: the class's columns were copied into item-ordered packed arrays at
+// upload (pack_columns): `colptr` / `rem` / the entry arrays are indexed by
+// list position, `list` only maps a position to its column for the q write.
+// Power-law models have millions of 1-16-entry columns scattered through the
+// store; packed, a warp step reads one contiguous run instead of a few
+// partially used sectors per column.
+template <class T, bool kPess, int SEG, bool kPacked = false>
 __global__ void __launch_bounds__(256)
 omax_tiny(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
           const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
@@ -664,9 +670,10 @@ omax_tiny(int nlist, const int* __restrict__ list, const long long* __restrict__
         r = T(0);
         if (st < nsteps && idx < nlist) {
             c = __ldg(list + idx);
-            b = __ldg(colptr + c);
-            L = static_cast<int>(__ldg(colptr + c + 1) - b);
-            r = __ldg(rem + c);
+            const int ci = kPacked ? idx : c;
+            b = __ldg(colptr + ci);
+            L = static_cast<int>(__ldg(colptr + ci + 1) - b);
+            r = __ldg(rem + ci);
         }
     };
     int c, L;
@@ -730,6 +737,26 @@ omax_tiny(int nlist, const int* __restrict__ list, const long long* __restrict__
         L = L2;
         r = r2;
         row = row2;
+    }
+}
+
+// Copies the columns of a class list into item-ordered packed arrays (see
+// omax_tiny's kPacked).  One thread per column (tiny columns: <= 16 entries).
+template <class T>
+__global__ void __launch_bounds__(256)
+pack_columns(int n, const int* __restrict__ list, const long long* __restrict__ colptr, const long long* __restrict__ pk_beg,
+             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+             const T* __restrict__ rem, int* __restrict__ pk_rows, T* __restrict__ pk_lower, T* __restrict__ pk_gap,
+             T* __restrict__ pk_rem) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int c = list[i];
+        const long long b = colptr[c], e = colptr[c + 1], o = pk_beg[i];
+        for (long long k = b; k < e; ++k) {
+            pk_rows[o + (k - b)] = rows[k];
+            pk_lower[o + (k - b)] = lower[k];
+            pk_gap[o + (k - b)] = gap[k];
+        }
+        pk_rem[i] = rem[c];
     }
 }
 
