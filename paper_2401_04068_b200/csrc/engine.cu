@@ -1194,12 +1194,25 @@ void launch_medium(rimdp_model* m, int count, const DevBuf& list, const T* V, T*
                                              m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), V, q, ctl, work);
 }
 
+// omax_tiny_rank (ranks + one replay of the consumed chain) by default; RIMDP_TINY=loop: omax_tiny's
+// repeated segment argmins.  Same bits either way.
+bool tiny_rank_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("RIMDP_TINY");
+        return !(e && strcmp(e, "loop") == 0);
+    }();
+    return on;
+}
+
 template <class T, int SEG>
 void launch_tiny(rimdp_model* m, const ColumnLists& L, int i, const T* V, T* q, Ctl* ctl, bool pess) {
     const int count = L.n_tiny[i];
     const bool pk = L.tiny_packed[i];
-    auto k = pk ? (pess ? omax_tiny<T, true, SEG, true> : omax_tiny<T, false, SEG, true>)
-                : (pess ? omax_tiny<T, true, SEG> : omax_tiny<T, false, SEG>);
+    auto k = tiny_rank_enabled()
+                 ? (pk ? (pess ? omax_tiny_rank<T, true, SEG, true> : omax_tiny_rank<T, false, SEG, true>)
+                       : (pess ? omax_tiny_rank<T, true, SEG> : omax_tiny_rank<T, false, SEG>))
+                 : (pk ? (pess ? omax_tiny<T, true, SEG, true> : omax_tiny<T, false, SEG, true>)
+                       : (pess ? omax_tiny<T, true, SEG> : omax_tiny<T, false, SEG>));
     static int per_sm[64] = {};
     const int dev = m->device & 63;
     if (!per_sm[dev]) {

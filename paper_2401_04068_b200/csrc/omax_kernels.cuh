@@ -740,6 +740,110 @@ omax_tiny(int nlist, const int* __restrict__ list, const long long* __restrict__
     }
 }
 
+// omax_tiny by ranks instead of repeated argmins.  Each lane counts its
+// entry's rank in its segment's (key, position) order (SEG independent
+// shuffles, no dependent chain), scatters its gap to that slot of the warp's
+// shared-memory row, and then every lane replays the reference's `consumed`
+// chain (omax.hpp:102-110) over the sorted gaps up to the end of the column,
+// taking avail at its own rank:
+//   avail_k = r - (g_(0) + ... + g_(k-1))   (sequential, as the reference)
+//   p       = avail_k > 0 ? l + min(g, avail_k) : l
+// avail is non-increasing along the chain (g >= 0), so "avail_k > 0" is the
+// reference's loop condition at step k.  The row-order dot is the segment
+// leader's sequential sum over the products staged in the same row.  Same
+// arithmetic as omax_tiny, so the same bits; about a third of its
+// instructions for columns with several picks.
+template <class T, bool kPess, int SEG, bool kPacked = false>
+__global__ void __launch_bounds__(256)
+omax_tiny_rank(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+               const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
+               const T* __restrict__ rem, const T* __restrict__ V, T* __restrict__ q, const Ctl* __restrict__ ctl) {
+    using N = Num<T>;
+    using Bits = typename N::Bits;
+    constexpr int CPW = 32 / SEG;
+    __shared__ __align__(16) T rowbuf[8][32];
+    pdl_enter_class(ctl);
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    const int lane = threadIdx.x & 31, sg = lane / SEG, sl = lane % SEG;
+    T* sb = rowbuf[threadIdx.x >> 5] + sg * SEG;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int nsteps = (nlist + CPW - 1) / CPW;
+    const unsigned long long pstream = l2_evict_first_policy(), pval = l2_evict_last_policy();
+    int step = gw;
+    if (step >= nsteps) return;
+    auto meta = [&](int st, int& c, long long& b, int& L, T& r) {
+        const int idx = st * CPW + sg;
+        c = -1;
+        b = 0;
+        L = 0;
+        r = T(0);
+        if (st < nsteps && idx < nlist) {
+            c = __ldg(list + idx);
+            const int ci = kPacked ? idx : c;
+            b = __ldg(colptr + ci);
+            L = static_cast<int>(__ldg(colptr + ci + 1) - b);
+            r = __ldg(rem + ci);
+        }
+    };
+    int c, L;
+    long long b;
+    T r;
+    meta(step, c, b, L, r);
+    int row = sl < L ? ld_hint(rows + b + sl, pstream) : 0;
+    for (;;) {
+        T l = T(0), g = T(0), v = T(0);
+        if (sl < L) {
+            l = ld_hint(lower + b + sl, pstream);
+            g = ld_hint(gap + b + sl, pstream);
+            v = ld_hint(V + row, pval);
+        }
+        const int nstep = step + nw;
+        int c2, L2;
+        long long b2;
+        T r2;
+        meta(nstep, c2, b2, L2, r2);
+        const int row2 = sl < L2 ? ld_hint(rows + b2 + sl, pstream) : 0;
+        // rank of the entry in the segment's (key, position) order
+        const Bits key = sl < L ? order_key<T>(v, kPess) : ~Bits(0);
+        int rank = 0;
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) {
+            const Bits kj = __shfl_sync(kFull, key, sg * SEG + j);
+            rank += (kj < key) | ((kj == key) & (j < sl));
+        }
+        if (sl < L) sb[rank] = g;
+        __syncwarp();
+        // the greedy's `consumed` chain over the sorted gaps; p at this lane's rank
+        T consumed = T(0), p = l;
+#pragma unroll
+        for (int k = 0; k < SEG; ++k) {
+            if (k < L) {
+                const T a = N::sub(r, consumed);
+                if (k == rank && a > T(0)) p = N::add(l, g < a ? g : a);
+                consumed = N::add(consumed, sb[k]);
+            }
+        }
+        __syncwarp();
+        sb[sl] = sl < L ? N::mul(v, p) : T(0);
+        __syncwarp();
+        if (sl == 0 && c >= 0) {
+            T acc = T(0);
+#pragma unroll
+            for (int i = 0; i < SEG; ++i)
+                if (i < L) acc = N::add(acc, sb[i]);
+            q[c] = acc;
+        }
+        __syncwarp();
+        step = nstep;
+        if (step >= nsteps) break;
+        c = c2;
+        b = b2;
+        L = L2;
+        r = r2;
+        row = row2;
+    }
+}
+
 // Copies the columns of a class list into item-ordered packed arrays (see
 // omax_tiny's kPacked).  One thread per column (tiny columns: <= 16 entries).
 template <class T>
