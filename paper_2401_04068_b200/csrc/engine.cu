@@ -318,11 +318,33 @@ int upload_threads() {
     return t;
 }
 
+// True when the whole range [p, p + bytes) is page-locked host memory (cudaHostAlloc / cudaHostRegister):
+// the copy engines then read it directly, no staging.
+bool pinned_host(const void* p, size_t bytes) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    if (a.type != cudaMemoryTypeHost || bytes == 0) return a.type == cudaMemoryTypeHost;
+    // a pinned allocation covers the last byte too (separately pinned neighbours would also pass, and are
+    // just as good for the DMA)
+    if (cudaPointerGetAttributes(&a, static_cast<const char*>(p) + bytes - 1) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 void upload_many(int device, cudaStream_t stream, const std::vector<UploadJob>& jobs) {
     size_t total = 0;
-    for (const auto& j : jobs) total += j.bytes;
+    bool all_pinned = true;
+    for (const auto& j : jobs) {
+        total += j.bytes;
+        if (j.bytes && all_pinned) all_pinned = pinned_host(j.src, j.bytes);
+    }
     const int W = upload_threads();
-    if (W == 0 || total < (32u << 20)) {
+    if (W == 0 || total < (32u << 20) || all_pinned) {
         for (const auto& j : jobs)
             if (j.bytes) CK(cudaMemcpyAsync(j.dst, j.src, j.bytes, cudaMemcpyHostToDevice, stream));
         return;
