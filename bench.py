@@ -272,6 +272,14 @@ def engine_arm(args, w):
         local = int(dmap.split(",")[local])
     torch.cuda.set_device(local)
     dist = None
+    if world > 1 and args.exchange == "peer":
+        # the fused exchange stores into the peers' HBM: every pair of the node's GPUs needs P2P access
+        # (NVLink / NVSwitch).  Without it every rank takes the NCCL path (the same check on every rank)
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        devs = [int(dmap.split(",")[r]) for r in range(local_world)] if dmap else list(range(local_world))
+        if any(a != b and not torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs):
+            log("[bench] no P2P access between the node's GPUs: NCCL exchange instead of the fused peer stores")
+            args.exchange = "nccl"
     if world > 1:
         import torch.distributed as dist
         # control plane only (IPC handle swap, barriers, max over ranks): gloo on host tensors.  The peer
