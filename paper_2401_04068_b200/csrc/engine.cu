@@ -1057,6 +1057,22 @@ FallbackSlots fallback_slots(rimdp_model* m, int cls, int count) {
     return f;
 }
 
+// columns per warp of the exact route's walk + dot: 2 (exact_dotg<2>, default) or RIMDP_EXACT_DOT=1 (exact_dot).
+// Four per warp measured slower (C5 f32 3.89 vs 3.50 ms: 64-entry chunks, a quarter of the loading lanes)
+int exact_dot_group() {
+    static const int g = [] {
+        const char* e = getenv("RIMDP_EXACT_DOT");
+        return e && atoi(e) == 1 ? 1 : 2;
+    }();
+    return g;
+}
+using ExactDotKernel = void (*)(int, const int*, const long long*, const float*, const float*, float*,
+                                const unsigned short*, const float*, float*, const Ctl*);
+ExactDotKernel exact_dot_kernel() {
+    const int g = exact_dot_group();
+    return g == 1 ? exact_dot : exact_dotg<2>;
+}
+
 template <class T, bool P, int LG>
 void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
     if constexpr (std::is_same<T, float>::value && LG <= 8) {
@@ -1095,7 +1111,7 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
         if (!configured[dev]) {
             CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem()));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], ks, Sh::NT, Sh::smem()));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dot_per_sm[dev], exact_dot, kExactDotWarps * 32, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dot_per_sm[dev], exact_dot_kernel(), kExactDotWarps * 32, 0));
             per_sm[dev] = std::max(per_sm[dev], 1);
             dot_per_sm[dev] = std::max(dot_per_sm[dev], 1);
             configured[dev] = true;
@@ -1111,7 +1127,8 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
                    list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(), m->gap.as<float>(), V,
                    m->xs_gap.as<float>(), m->xs_pos.as<unsigned short>(), m->xs_val.as<float>(), f.list, f.count,
                    f.other, (const Ctl*)ctl);
-        launch_pdl(m->pdl_wait_ok(), exact_dot, grid_for(count, kExactDotWarps, m->sm_count, dot_per_sm[dev]),
+        const int G = exact_dot_group();
+        launch_pdl(m->pdl_wait_ok(), exact_dot_kernel(), grid_for((count + G - 1) / G, kExactDotWarps, m->sm_count, dot_per_sm[dev]),
                    kExactDotWarps * 32, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
                    m->lower.as<float>(), m->rem.as<float>(), m->xs_gap.as<float>(),
                    (const unsigned short*)m->xs_pos.as<unsigned short>(), (const float*)m->xs_val.as<float>(), q,

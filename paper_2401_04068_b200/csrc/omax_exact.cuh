@@ -376,6 +376,154 @@ exact_dot(int nlist, const int* __restrict__ list, const long long* __restrict__
     }
 }
 
+// exact_dot with G columns per warp (G = 2: lanes 0-15 take list item 2p,
+// lanes 16-31 item 2p + 1), each lane holding 8 entries of its group's
+// chunk of CH = 8 x 32/G entries.  The serial chains (the walk's `consumed`,
+// the row-order dot) run on the G group leaders side by side, so every
+// serial warp instruction advances G columns — the single-column kernel is
+// issue-bound (80% issue-active) on exactly those chains.  The class lists
+// are sorted by length, so the columns of a warp need about as many chunks.
+// Same arithmetic in the same order as exact_dot: the same bits.
+template <int G>
+__global__ void __launch_bounds__(kExactDotWarps * 32)
+exact_dotg(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
+           const float* __restrict__ lower, const float* __restrict__ rem, float* __restrict__ S,
+           const unsigned short* __restrict__ POS, const float* __restrict__ VS, float* __restrict__ q,
+           const Ctl* __restrict__ ctl) {
+    using N_ = Num<float>;
+    constexpr int U = 8;       // entries per lane per chunk
+    constexpr int LPC = 32 / G; // lanes per column
+    constexpr int CH = U * LPC; // chunk
+    pdl_enter();
+    if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
+    __shared__ __align__(16) float buf[kExactDotWarps][G][CH];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, h = lane / LPC, hl = lane % LPC;
+    float* sb = buf[w][h];
+    const int ngroups = (nlist + G - 1) / G;
+    for (int pr = blockIdx.x * kExactDotWarps + w; pr < ngroups; pr += gridDim.x * kExactDotWarps) {
+        const int item = G * pr + h;
+        const bool valid = item < nlist;
+        const int c = valid ? list[item] : 0;
+        const long long b0 = valid ? colptr[c] : 0;
+        const int L = valid ? static_cast<int>(colptr[c + 1] - b0) : 0;
+        const float r = valid ? rem[c] : 0.f;
+        // ---- the greedy (omax.hpp:102-110) along the sorted gaps, CH at a time per group ----
+        float consumed = 0.f;
+        int J = L;
+        float gv[U], gn[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = u * LPC + hl;
+            gv[u] = j < L ? S[b0 + j] : 0.f;
+        }
+        double P = 0.0;
+        bool walking = L > 0;
+        for (int j0 = 0; __any_sync(kFull, walking); j0 += CH) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) sb[u * LPC + hl] = gv[u];
+            double cs = 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) cs += (double)gv[u];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + CH + u * LPC + hl;
+                gn[u] = walking && j < L ? S[b0 + j] : 0.f;
+            }
+#pragma unroll
+            for (int o = LPC / 2; o > 0; o >>= 1) cs += __shfl_xor_sync(kFull, cs, o);
+            const int m = L - j0 < CH ? L - j0 : CH;
+            P += cs;
+            // fast chunk (see exact_dot): every entry is a full pick, only the chain runs
+            const bool fast = walking && P * (1.0 + 1.02 * (double)(j0 + m) * 0x1p-24) < (double)r;
+            __syncwarp();
+            int picks = m;
+            if (walking && hl == 0) {
+                if (fast) {
+                    const float4* s4 = reinterpret_cast<const float4*>(sb);
+                    const int m4 = m >> 2;
+#pragma unroll 8
+                    for (int k = 0; k < m4; ++k) {
+                        const float4 g4 = s4[k];
+                        consumed = N_::add(consumed, g4.x);
+                        consumed = N_::add(consumed, g4.y);
+                        consumed = N_::add(consumed, g4.z);
+                        consumed = N_::add(consumed, g4.w);
+                    }
+                    for (int k = m4 * 4; k < m; ++k) consumed = N_::add(consumed, sb[k]);
+                } else {
+                    picks = exact_walk_chunk(sb, m, r, consumed);
+                }
+            }
+            picks = __shfl_sync(kFull, picks, h * LPC);
+            __syncwarp();
+            if (walking && !fast) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = u * LPC + hl;
+                    if (k < picks) S[b0 + j0 + k] = sb[k];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) gv[u] = gn[u];
+            __syncwarp();
+            if (walking && picks < m) {
+                J = j0 + picks;
+                walking = false;
+            } else if (walking && j0 + CH >= L) {
+                walking = false;
+            }
+        }
+        // ---- row-order expectation (omax.hpp:169-173), CH products at a time per group ----
+        int Lmax = L;
+#pragma unroll
+        for (int o = LPC; o < 32; o <<= 1) Lmax = max(Lmax, __shfl_xor_sync(kFull, Lmax, o));
+        float dot = 0.f;
+        int sp[U];
+        float lw[U], vw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = u * LPC + hl;
+            sp[u] = i < L ? POS[b0 + i] : 0x7fffffff;
+            lw[u] = i < L ? __ldg(lower + b0 + i) : 0.f;
+            vw[u] = i < L ? VS[b0 + i] : 0.f;
+        }
+        for (int i0 = 0; i0 < Lmax; i0 += CH) {
+            float x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const float ex = sp[u] < J ? S[b0 + sp[u]] : 0.f;
+                x[u] = N_::mul(vw[u], sp[u] < J ? N_::add(lw[u], ex) : lw[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + CH + u * LPC + hl;
+                sp[u] = i < L ? POS[b0 + i] : 0x7fffffff;
+                lw[u] = i < L ? __ldg(lower + b0 + i) : 0.f;
+                vw[u] = i < L ? VS[b0 + i] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) sb[u * LPC + hl] = x[u];
+            __syncwarp();
+            if (hl == 0 && i0 < L) {
+                const int m = L - i0 < CH ? L - i0 : CH;
+                const float4* s4 = reinterpret_cast<const float4*>(sb);
+                const int m4 = m >> 2;
+#pragma unroll 8
+                for (int k = 0; k < m4; ++k) {
+                    const float4 v = s4[k];
+                    dot = N_::add(dot, v.x);
+                    dot = N_::add(dot, v.y);
+                    dot = N_::add(dot, v.z);
+                    dot = N_::add(dot, v.w);
+                }
+                for (int k = m4 * 4; k < m; ++k) dot = N_::add(dot, sb[k]);
+            }
+            __syncwarp();
+        }
+        if (hl == 0 && valid) q[c] = dot;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Columns of 33 .. 256 entries in one pass, one warp per column
 // (exact_warp): the same sort, greedy walk and row-order dot as exact_sort +
