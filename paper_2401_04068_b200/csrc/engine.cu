@@ -1084,6 +1084,7 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
         const int dev = m->device & 63;
         if (!configured[dev]) {
             CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem()));
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k, Sh::W * 32, Sh::smem()));
             per_sm[dev] = std::max(per_sm[dev], 1);
             configured[dev] = true;

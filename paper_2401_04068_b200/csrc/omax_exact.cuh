@@ -536,6 +536,11 @@ struct ExactWarpShape {
     static constexpr int N = 1 << LG;   // 64 .. 256
     static constexpr int E = N / 32;    // entries per lane
     static constexpr int W = 8;         // warps per block
+#ifndef RIMDP_EXACT_WARP_MINBLOCKS
+#define RIMDP_EXACT_WARP_MINBLOCKS 3
+#endif
+    // 256 entries: 3 blocks per SM (<= 85 registers) instead of the 2 that 90 registers allow
+    static constexpr int MinBlocks = LG >= 8 ? RIMDP_EXACT_WARP_MINBLOCKS : 1;
     // per warp: tmp u64[N] (then the dot's staging buffer) | cnt u32[N + 4] | S f32[N]; each lane keeps its
     // entries' V, lower, gap and sorted position in registers
     static constexpr size_t warp_bytes = (size_t)N * 8 + (size_t)(N + 4) * 4 + (size_t)N * 4;
@@ -543,7 +548,7 @@ struct ExactWarpShape {
 };
 
 template <bool kPess, int LG>
-__global__ void __launch_bounds__(ExactWarpShape<LG>::W * 32)
+__global__ void __launch_bounds__(ExactWarpShape<LG>::W * 32, ExactWarpShape<LG>::MinBlocks)
 exact_warp(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
            const int* __restrict__ rows, const float* __restrict__ lower, const float* __restrict__ gap,
            const float* __restrict__ rem, const float* __restrict__ V, float* __restrict__ q,
