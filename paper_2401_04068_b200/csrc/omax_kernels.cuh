@@ -2391,16 +2391,26 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             pa[wig] = bs;
             pb[wig] = acc;
         }
-        __syncthreads(); // B4: partials and candidates complete
+        // The last warp to get here completes the column; the others go on to
+        // the next one at once (no block barrier: an arrival counter, dw[2],
+        // with CTA-scope fences on both sides).  The shared state it reads —
+        // partials, candidates, dw — is rewritten only after the next
+        // column's B1, which this warp reaches after finishing.
+        __threadfence_block();
+        __syncwarp();
+        unsigned last = 0;
+        if (lane == 0) last = atomicAdd(reinterpret_cast<unsigned*>(dw + 2), 1u) == static_cast<unsigned>(NW - 1);
+        last = __shfl_sync(kFull, last, 0);
         par ^= 1u;
-        const int K = picks ? dw[3] : 0;
+        if (!last) continue;
+        __threadfence_block();
+        const int K = picks ? *reinterpret_cast<volatile int*>(dw + 3) : 0;
         if (K > CAP) {
             // too many entries in the bracket (ties, clustered values): selection kernel
-            if (t == 0) fallback[atomicAdd(nfallback, 1)] = c;
+            if (lane == 0) fallback[atomicAdd(nfallback, 1)] = c;
             continue;
         }
-        if (wig != 0) continue;
-        // ---- warp 0: the greedy (omax.hpp:98-112) inside the bracket, q ----
+        // ---- the last warp: the greedy (omax.hpp:98-112) inside the bracket, q ----
         // Two candidates per lane (slots lane, 32 + lane).  `consumed` starts
         // at the exact base below the bracket and grows along the adversary
         // order: each pick is the exact warp argmin over (order key, position),
