@@ -2109,10 +2109,11 @@ omax_select(int nlist, const int* __restrict__ list, const long long* __restrict
 // accumulated in shared memory as fixed-point integers (g * Sc truncated,
 // Sc = 2^31 / (L * max gap): no overflow; integer atomics, deterministic).
 // Since truncation loses < 1 unit per entry, the exact mass before bucket b
-// lies in [F_b, F_b + N_b) (fixed mass and count before b), which brackets the
-// bucket of the cut c (the last entry whose prefix gap mass is < rem) in
-// [b_lo, b_hi]:  b_lo = last non-empty bucket with F_b + N_b <= rem * Sc
-// (certainly reached), b_hi = last non-empty bucket with F_b < rem * Sc.
+// lies in [F_b, F_b + L) (F_b the fixed mass before b, L the column length),
+// which brackets the bucket of the cut c (the last entry whose prefix gap
+// mass is < rem) in [b_lo, b_hi]:  b_lo = last bucket with F_b + L <= rem * Sc
+// (certainly reached), b_hi = last bucket with F_b < rem * Sc.  (Empty
+// buckets in the bracket hold no entries; no count histogram is needed.)
 // Entries below b_lo are before c: their exact gap sum (double, tree order)
 // is the base, and their V g is added to the expectation.  The <= kBucketCap
 // entries of [b_lo, b_hi] are resolved exactly by warp 0: bitonic sort by
@@ -2140,9 +2141,9 @@ struct BucketShape {
     static constexpr int MinBlocks = NT >= 1024 ? 1 : 1024 / NT;
     template <class T>
     static constexpr size_t smem() {
-        // hist, cnt (u32 x B) x 2 (alternate columns); candidates (key, pos, g, V) x kBucketCap; partials
+        // hist (u32 x B) x 2 (alternate columns); candidates (key, pos, g, V) x kBucketCap; partials
         // (sum g below the bracket, sum V l + V g below) x NW; warp scan totals; decision words x 2
-        return 2 * 2 * 4 * B + kBucketCap * (8 + 4 + 2 * sizeof(T)) + NW * (2 * sizeof(T) + 16) + 64;
+        return 2 * 4 * B + kBucketCap * (8 + 4 + 2 * sizeof(T)) + NW * (2 * sizeof(T) + 16) + 64;
     }
 };
 
@@ -2186,23 +2187,24 @@ value_range(int n, const T* __restrict__ V, unsigned long long* __restrict__ slo
 // cannot occur; the index is clamped anyway.  A fixed-point gap histogram
 // uses u32 shared atomics at a scale chosen per column so it cannot
 // overflow; it is deterministic.  Since truncation loses < 1 unit per entry,
-// the exact mass before bucket b lies in [F_b, F_b + N_b) (fixed mass and
-// count before b), which brackets the bucket of the cut c (the last entry
-// whose prefix gap mass is < rem) in [b_lo, b_hi]:  b_lo = last non-empty
-// bucket with F_b + N_b <= rem * Sc (certainly reached), b_hi = last
-// non-empty bucket with F_b < rem * Sc.  Entries below b_lo are before c:
-// their exact gap sum (double, tree order) is the base, and their V g is
-// added to the expectation.  The <= kBucketCap entries of [b_lo, b_hi] are
-// resolved exactly by warp 0: bitonic sort by (order key, position),
-// exclusive prefix of the gaps from the base, the cut is the last entry
-// whose prefix is < rem.
+// the exact mass before bucket b lies in [F_b, F_b + L) (F_b the fixed mass
+// before b), which brackets the bucket of the cut c (the last entry whose
+// prefix gap mass is < rem) in [b_lo, b_hi]:  b_lo = last bucket with
+// F_b + L <= rem * Sc (certainly reached), b_hi = last bucket with
+// F_b < rem * Sc; the fixed-point total is <= 2^31, so the scan is 32-bit.
+// Entries below b_lo are before c: their exact gap sum (double, tree order)
+// is the base, and their V g is added to the expectation.  The <= kBucketCap
+// entries of [b_lo, b_hi] are resolved exactly by the greedy itself, run by
+// the last warp to finish the column: exact warp argmins over (order key,
+// position), `consumed` continued sequentially from the base.
 //   q = sum V l + sum_{before c} V g + V_c min(g_c, rem - F(c))
 // A column whose bracket holds more than kBucketCap entries (heavy ties,
 // clustered values) is appended to a fallback list for omax_select.  Sums are
 // in tree order: within a few ulps of the reference (1e-12 tests).
-// Four barriers per column (histogram, scan, bracket, partials); the
-// histogram and the decision words alternate between two buffers so the
-// next column needs no trailing barrier.
+// Three barriers per column (histogram, scan, bracket); the last warp to
+// deposit its partials completes the column (arrival counter), the others
+// go on; the histogram and the decision words alternate between two buffers
+// so the next column needs no trailing barrier.
 template <class T, bool kPess, int LG>
 __global__ void __launch_bounds__(BucketShape<LG, T>::NT, BucketShape<LG, T>::MinBlocks)
 omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
@@ -2221,8 +2223,8 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
     if (blockIdx.x == 0 && threadIdx.x == 0) *other_nfallback = 0;
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned* hbuf = reinterpret_cast<unsigned*>(smem_raw);           // [2][hist B | cnt B]
-    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hbuf + 4 * B);
+    unsigned* hbuf = reinterpret_cast<unsigned*>(smem_raw);           // [2][hist B]
+    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hbuf + 2 * B);
     T* cg = reinterpret_cast<T*>(ckey + CAP);
     T* cv = cg + CAP;
     int* cpos = reinterpret_cast<int*>(cv + CAP);
@@ -2255,8 +2257,7 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
         const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
         const T r = __ldg(rem + c);
         const bool picks = r > T(0);
-        unsigned* hist = hbuf + par * 2 * B;
-        unsigned* hcnt = hist + B;
+        unsigned* hist = hbuf + par * B;
         int* dw = dwb + par * 4;
         // ---- load (registers); sum V l; fixed-point gap histogram ----
         int rw[E];
@@ -2293,66 +2294,47 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
         if (picks) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                if (e * NT + t < L) {
-                    const int bb = bucket_of(v[e]);
-                    atomicAdd(hist + bb, static_cast<unsigned>((double)g[e] * sc));
-                    atomicAdd(hcnt + bb, 1u);
-                }
+                if (e * NT + t < L) atomicAdd(hist + bucket_of(v[e]), static_cast<unsigned>((double)g[e] * sc));
             }
         }
         __syncthreads(); // B1: histogram complete
         {   // the next column's buffers: their last readers (the previous column) are past B1
-            unsigned* oh = hbuf + (par ^ 1u) * 2 * B;
-            for (int i = t; i < 2 * B; i += NT) oh[i] = 0u;
+            unsigned* oh = hbuf + (par ^ 1u) * B;
+            for (int i = t; i < B; i += NT) oh[i] = 0u;
             if (t < 4) dwb[(par ^ 1u) * 4 + t] = 0;
         }
         T bs = T(0);
         if (picks) {
             // ---- bracket of the cut's bucket: block-wide exclusive scan of the buckets ----
+            // (the fixed-point total is <= 2^31: 32-bit prefixes)
             constexpr int PB = B / NT > 0 ? B / NT : 1; // buckets per thread
-            unsigned long long fm = 0, fn = 0;
+            unsigned fm = 0;
 #pragma unroll
             for (int i = 0; i < PB; ++i) {
                 const int bb = t * PB + i;
-                if (bb < B) {
-                    fm += hist[bb];
-                    fn += hcnt[bb];
-                }
+                if (bb < B) fm += hist[bb];
             }
-            unsigned long long em = fm, en = fn;
+            unsigned em = fm;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long a = __shfl_up_sync(kFull, em, o), z = __shfl_up_sync(kFull, en, o);
-                if (lane >= o) {
-                    em += a;
-                    en += z;
-                }
+                const unsigned a = __shfl_up_sync(kFull, em, o);
+                if (lane >= o) em += a;
             }
-            if (lane == 31) {
-                wtot[wig] = em;
-                wtot[NW + wig] = en;
-            }
+            if (lane == 31) wtot[wig] = em;
             __syncthreads(); // B2
             em -= fm;
-            en -= fn;
-            for (int i = 0; i < wig; ++i) {
-                em += wtot[i];
-                en += wtot[NW + i];
-            }
+            for (int i = 0; i < wig; ++i) em += static_cast<unsigned>(wtot[i]);
             {
-                const double R = (double)r * sc;
+                // truncation lost < 1 unit per entry, < L before any bucket
+                const double R = (double)r * sc, RL = R - (double)L;
                 int blo = -1, bhi = -1;
 #pragma unroll
                 for (int i = 0; i < PB; ++i) {
                     const int bb = t * PB + i;
                     if (bb < B) {
-                        const unsigned hm = hist[bb], hn = hcnt[bb];
-                        if (hn > 0) {
-                            if ((double)(em + en) <= R) blo = bb;
-                            if ((double)em < R) bhi = bb;
-                        }
-                        em += hm;
-                        en += hn;
+                        if ((double)em <= RL) blo = bb;
+                        if ((double)em < R) bhi = bb;
+                        em += hist[bb];
                     }
                 }
                 if (blo >= 0) atomicMax(dw + 0, blo + 1);
@@ -2480,7 +2462,7 @@ struct WBucketShape {
     static constexpr int B = Len / 4;           // 16, 32, 64
     static constexpr int PB = B >= 32 ? B / 32 : 1;
     static constexpr int W = 8;                 // warps per block
-    static constexpr int WarpBytes = 2 * 4 * B + 32 * (8 + 2 * 8);
+    static constexpr int WarpBytes = 4 * B + 32 * (8 + 2 * 8);
 };
 
 template <class T, bool kPess, int LG>
@@ -2500,8 +2482,7 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
     __shared__ __align__(16) unsigned char smem[W * Sh::WarpBytes];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned* hist = reinterpret_cast<unsigned*>(smem + w * Sh::WarpBytes);
-    unsigned* hcnt = hist + B;
-    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hcnt + B);
+    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hist + B);
     T* cg = reinterpret_cast<T*>(ckey + 32);
     T* cv = cg + 32;
     const unsigned lt = (1u << lane) - 1u;
@@ -2547,53 +2528,39 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
         if (picks) {
             // ---- fixed-point gap histogram (warp-private) ----
 #pragma unroll
-            for (int i = lane; i < 2 * B; i += 32) hist[i] = 0u;
+            for (int i = lane; i < B; i += 32) hist[i] = 0u;
             __syncwarp();
             const T gm = __ldg(maxgap + c);
             const double sc = gm > T(0) ? 2147483648.0 / ((double)L * (double)gm) : 0.0;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                if (e * 32 + lane < L) {
-                    const int bb = bucket_of(v[e]);
-                    atomicAdd(hist + bb, static_cast<unsigned>((double)g[e] * sc));
-                    atomicAdd(hcnt + bb, 1u);
-                }
+                if (e * 32 + lane < L) atomicAdd(hist + bucket_of(v[e]), static_cast<unsigned>((double)g[e] * sc));
             }
             __syncwarp();
             // ---- bracket: warp scan of the buckets (lane owns PB consecutive buckets) ----
-            unsigned fm = 0, fn = 0;
+            unsigned fm = 0;
 #pragma unroll
             for (int i = 0; i < PB; ++i) {
                 const int bb = lane * PB + i;
-                if (bb < B) {
-                    fm += hist[bb];
-                    fn += hcnt[bb];
-                }
+                if (bb < B) fm += hist[bb];
             }
-            unsigned em = fm, en = fn;
+            unsigned em = fm;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const unsigned a = __shfl_up_sync(kFull, em, o), z = __shfl_up_sync(kFull, en, o);
-                if (lane >= o) {
-                    em += a;
-                    en += z;
-                }
+                const unsigned a = __shfl_up_sync(kFull, em, o);
+                if (lane >= o) em += a;
             }
             em -= fm;
-            en -= fn;
-            const double R = (double)r * sc;
+            // truncation lost < 1 unit per entry, < L before any bucket
+            const double R = (double)r * sc, RL = R - (double)L;
             int blo = -1, bhi = -1;
 #pragma unroll
             for (int i = 0; i < PB; ++i) {
                 const int bb = lane * PB + i;
                 if (bb < B) {
-                    const unsigned hm = hist[bb], hn = hcnt[bb];
-                    if (hn > 0) {
-                        if ((double)em + (double)en <= R) blo = bb;
-                        if ((double)em < R) bhi = bb;
-                    }
-                    em += hm;
-                    en += hn;
+                    if ((double)em <= RL) blo = bb;
+                    if ((double)em < R) bhi = bb;
+                    em += hist[bb];
                 }
             }
             const int lo_b = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(blo + 1)));
