@@ -1127,7 +1127,7 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
         launch_pdl(m->pdl_now, ks, grid_for(count, 1, m->sm_count, per_sm[dev]), Sh::NT, Sh::smem(), m->ls, count,
                    list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(), m->gap.as<float>(), V,
                    m->xs_gap.as<float>(), m->xs_pos.as<unsigned short>(), m->xs_val.as<float>(), f.list, f.count,
-                   f.other, (const Ctl*)ctl);
+                   f.other, (const Ctl*)ctl, m->vrange_cur);
         const int G = exact_dot_group();
         launch_pdl(m->pdl_wait_ok(), exact_dot_kernel(), grid_for((count + G - 1) / G, kExactDotWarps, m->sm_count, dot_per_sm[dev]),
                    kExactDotWarps * 32, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
@@ -1395,14 +1395,14 @@ void launch_sorted_fanout(rimdp_model* m, const ColumnLists& L, const T* V, T* q
 }
 
 // Per-column expectations q for the columns of one set of class lists.
-// Range of V for the value buckets of omax_bucket: one small launch per
-// column pass, only when a bucket class is scheduled.
+// Range of V for the value buckets of omax_bucket and exact_sort: one small
+// launch per column pass, only when such a class is scheduled.
 template <class T>
 void launch_value_range(rimdp_model* m, const ColumnLists& L, const T* V) {
     bool need = false;
     for (int i = 0; i < kSortedClasses; ++i) need = need || L.n_sorted[i] > 0;
     m->vrange_cur = nullptr;
-    if (!need || m->bitonic || m->exact_sorted || !m->bucket) return;
+    if (!need || m->bitonic || !(m->exact_sorted || m->bucket)) return;
     if (!m->vrange.p) {
         m->vrange.ensure(4 * sizeof(unsigned long long));
         const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};

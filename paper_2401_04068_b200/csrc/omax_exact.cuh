@@ -88,7 +88,7 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
            const int* __restrict__ rows, const float* __restrict__ gap, const float* __restrict__ V,
            float* __restrict__ S, unsigned short* __restrict__ POS, float* __restrict__ VS,
            int* __restrict__ fb_list, int* __restrict__ fb_count, int* __restrict__ fb_other,
-           const Ctl* __restrict__ ctl) {
+           const Ctl* __restrict__ ctl, const unsigned long long* __restrict__ vrange) {
     using Sh = ExactShape<LG>;
     constexpr int N = Sh::N, NT = Sh::NT, E = Sh::E;
     pdl_enter_class(ctl);
@@ -99,24 +99,30 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned* cnt = reinterpret_cast<unsigned*>(smem_raw);                                       // N + 1
     unsigned long long* tmp = reinterpret_cast<unsigned long long*>(smem_raw + ((N + 1) * 4 + 15) / 16 * 16);
-    __shared__ unsigned kmin_s, kmax_s, wsum[32];
+    __shared__ unsigned wsum[32];
     __shared__ int over;
     const int tid = threadIdx.x;
+    // equal-width buckets over the value vector's range (value_range, one launch per iteration), in
+    // adversary order (w = V pessimistic, -V optimistic): fl(w - w_min) * scale truncated is
+    // non-decreasing in w, so buckets are contiguous in the (key, position) order and equal values share
+    // one.  (Buckets over the order keys would not do: the keys of float values are logarithmic, so half
+    // of [0, 1) would land in 1/24 of them.)  A column sampling random states spreads over about the
+    // whole range, ~1 entry per bucket.
+    const float vlo = value_of_key<float>(static_cast<unsigned>(__ldg(vrange)), true);
+    const float vhi = value_of_key<float>(static_cast<unsigned>(__ldg(vrange + 1)), true);
+    const float wmin = kPess ? vlo : -vhi, wmax = kPess ? vhi : -vlo;
+    const float width = __fsub_rn(wmax, wmin);
+    const float scale = width > 0.f && width < 3.0e38f ? __fdiv_rn(static_cast<float>(N), width) : 0.f;
     for (int item = blockIdx.x; item < nlist; item += gridDim.x) {
         const int c = list[item];
         const long long b0 = colptr[c];
         const int L = static_cast<int>(colptr[c + 1] - b0);
         for (int k = tid; k <= N; k += NT) cnt[k] = 0u;
-        if (tid == 0) {
-            kmin_s = ~0u;
-            kmax_s = 0u;
-        }
         __syncthreads();
         // every read of the previous column's flag happened before the barrier above (racecheck-clean)
         if (tid == 0) over = 0;
         unsigned key[E];
         float g[E];
-        unsigned lmin = ~0u, lmax = 0u;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int j = tid + e * NT;
@@ -127,25 +133,8 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
                 VS[b0 + j] = v;
                 g[e] = __ldg(gap + b0 + j);
                 key[e] = static_cast<unsigned>(order_key<float>(v, kPess));
-                lmin = key[e] < lmin ? key[e] : lmin;
-                lmax = key[e] > lmax ? key[e] : lmax;
             }
         }
-        lmin = __reduce_min_sync(kFull, lmin);
-        lmax = __reduce_max_sync(kFull, lmax);
-        if ((tid & 31) == 0) {
-            atomicMin(&kmin_s, lmin);
-            atomicMax(&kmax_s, lmax);
-        }
-        __syncthreads();
-        // equal-width buckets over the column's value range, in adversary order (w = V pessimistic, -V
-        // optimistic): fl(w - w_min) * scale truncated is non-decreasing in w, so buckets are contiguous in
-        // the (key, position) order and equal values share one.  (Buckets over the order keys would not
-        // do: the keys of float values are logarithmic, so half of [0, 1) would land in 1/24 of them.)
-        const float vlo = value_of_key<float>(kmin_s, kPess), vhi = value_of_key<float>(kmax_s, kPess);
-        const float wmin = kPess ? vlo : -vlo, wmax = kPess ? vhi : -vhi;
-        const float width = __fsub_rn(wmax, wmin);
-        const float scale = width > 0.f && width < 3.0e38f ? __fdiv_rn(static_cast<float>(N), width) : 0.f;
         int bk[E];
         unsigned slot[E];
 #pragma unroll
