@@ -512,7 +512,7 @@ int long_mode() {
 //   4 + i: sorted, size class 2^(kSortedMinLog + i)
 //   kClassTiny + i: <= 4 << i entries (i = 0, 1, 2), several columns per warp
 constexpr int kClassMedium = 2, kClassSorted = 4, kClassTiny = 16;
-int column_class(long long len, double rem, double maxgap, int mode) {
+__host__ __device__ int column_class(long long len, double rem, double maxgap, int mode) {
     if (len <= 4) return kClassTiny;
     if (len <= 8) return kClassTiny + 1;
     if (len <= 16) return kClassTiny + 2;
@@ -538,11 +538,22 @@ int column_class(long long len, double rem, double maxgap, int mode) {
 
 // by_length: sort each many-pick class list by decreasing length (longest first balances the persistent
 // grids of the float32 exact route)
-void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>& cols, const std::vector<signed char>& cls,
+// cols == nullptr: every column, in order
+void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>* cols, const std::vector<signed char>& cls,
                 const long long* by_length = nullptr) {
     std::vector<int> sh, ex, md[2], ti[3], so[kSortedClasses];
-    if (!cols.empty() && cls[cols.front()] == 0 && cls[cols.back()] == 0) sh.reserve(cols.size());
-    for (int c : cols) {
+    const int n = cols ? (int)cols->size() : (int)cls.size();
+    {   // exact sizes first: one pass counting the classes
+        long long cnt[32] = {};
+        for (int i = 0; i < n; ++i) ++cnt[cls[cols ? (*cols)[i] : i] & 31];
+        sh.reserve(cnt[0]);
+        ex.reserve(cnt[1]);
+        for (int i = 0; i < 2; ++i) md[i].reserve(cnt[kClassMedium + i]);
+        for (int i = 0; i < 3; ++i) ti[i].reserve(cnt[kClassTiny + i]);
+        for (int i = 0; i < kSortedClasses; ++i) so[i].reserve(cnt[kClassSorted + i]);
+    }
+    for (int i = 0; i < n; ++i) {
+        const int c = cols ? (*cols)[i] : i;
         const int k = cls[c];
         if (k == 0) sh.push_back(c);
         else if (k >= kClassTiny) ti[k - kClassTiny].push_back(c);
@@ -630,6 +641,39 @@ void pack_tiny(rimdp_model* m, ColumnLists& L, const long long* h_colptr) {
     }
 }
 
+// column_class of every column on the device (rem / maxgap are device-computed, so the host would need
+// them copied back: 16 B per column against the 1-byte class), plus the longest column and the count and
+// total length of the short class (omax_pair's test): stat = [max length, short count, short entries]
+template <class T>
+__global__ void __launch_bounds__(256)
+classify_columns(int ncols, const long long* __restrict__ colptr, const T* __restrict__ rem,
+                 const T* __restrict__ maxgap, int mode, int any_long, signed char* __restrict__ cls,
+                 unsigned long long* __restrict__ stat) {
+    unsigned long long mx = 0, cnt = 0, tot = 0;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+        const long long len = colptr[c + 1] - colptr[c];
+        const int k = column_class(len, any_long ? (double)rem[c] : 0.0, any_long ? (double)maxgap[c] : 0.0, mode);
+        cls[c] = static_cast<signed char>(k);
+        mx = static_cast<unsigned long long>(len) > mx ? static_cast<unsigned long long>(len) : mx;
+        if (k == 0) {
+            ++cnt;
+            tot += static_cast<unsigned long long>(len);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(stat, mx);
+        atomicAdd(stat + 1, cnt);
+        atomicAdd(stat + 2, tot);
+    }
+}
+
 template <class T>
 void build_schedule(rimdp_model* m, const long long* h_colptr) {
     PhaseTrace tr("schedule");
@@ -638,13 +682,6 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     // columns (config 2) skip the device -> host copy of rem / maxgap
     bool any_long = false;
     for (int c = 0; c < m->ncols && !any_long; ++c) any_long = h_colptr[c + 1] - h_colptr[c] > kShortLen;
-    std::vector<T> h_rem(any_long ? m->ncols : 0), h_maxgap(any_long ? m->ncols : 0);
-    if (m->ncols > 0 && any_long) {
-        CK(cudaMemcpyAsync(h_rem.data(), m->rem.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
-        CK(cudaMemcpyAsync(h_maxgap.data(), m->maxgap.p, sizeof(T) * m->ncols, cudaMemcpyDeviceToHost, m->stream));
-        CK(cudaStreamSynchronize(m->stream));
-    }
-    tr.mark("d2h");
     const int mode = long_mode();
     m->bitonic = mode == 2;
     m->long_exact = mode == 1;
@@ -660,16 +697,25 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         const char* eb = getenv("RIMDP_BUCKET");
         m->bucket = !(eb && atoi(eb) == 0) && mode != 3;
     }
+    // classes on the device, one byte per column back to the host
     std::vector<signed char> cls(m->ncols);
-    std::vector<int> allc(m->ncols), qc;
-    int maxlen = 0;
-    for (int c = 0; c < m->ncols; ++c) {
-        const long long len = h_colptr[c + 1] - h_colptr[c];
-        maxlen = (int)std::max<long long>(maxlen, len);
-        cls[c] = (signed char)column_class(len, any_long ? (double)h_rem[c] : 0.0,
-                                           any_long ? (double)h_maxgap[c] : 0.0, mode);
-        allc[c] = c;
+    unsigned long long stat[3] = {0, 0, 0};
+    if (m->ncols > 0) {
+        DevBuf dcls, dstat;
+        dcls.ensure(m->ncols);
+        dstat.ensure(sizeof stat);
+        CK(cudaMemsetAsync(dstat.p, 0, sizeof stat, m->stream));
+        classify_columns<T><<<grid_for(m->ncols, 256, m->sm_count, 8), 256, 0, m->stream>>>(
+            m->ncols, m->colptr.as<long long>(), m->rem.as<T>(), m->maxgap.as<T>(), mode, any_long ? 1 : 0,
+            dcls.as<signed char>(), dstat.as<unsigned long long>());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(cls.data(), dcls.p, m->ncols, cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaMemcpyAsync(stat, dstat.p, sizeof stat, cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
     }
+    tr.mark("d2h");
+    const int maxlen = static_cast<int>(stat[0]);
+    std::vector<int> allc, qc;
     const std::vector<int>& sp = m->h_stateptr;
     const char* fz = getenv("RIMDP_FUSED");
     const bool fused = fz && atoi(fz) != 0;
@@ -711,26 +757,24 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
         bstates.back().y += 1;
     }
     close_batch();
-    if (!fused) qc = allc;
+    if (fused) {
+        allc.resize(m->ncols);
+        for (int c = 0; c < m->ncols; ++c) allc[c] = c;
+    }
     tr.mark("classify");
     m->maxlen = maxlen;
     {   // omax_pair pays off when the two columns of a step are nearly full (config 2: all 32 entries); with
         // the mixed 17-32 lengths of a power-law model (mean ~24) the pair's loop runs the longer column's
         // picks for both and measured 2% slower than omax_short
-        long long cnt = 0, tot = 0;
-        for (int c = 0; c < m->ncols; ++c)
-            if (cls[c] == 0) {
-                ++cnt;
-                tot += h_colptr[c + 1] - h_colptr[c];
-            }
+        const unsigned long long cnt = stat[1], tot = stat[2];
         m->short_pair = cnt == 0 || tot >= 28 * cnt;
     }
     // every column on the q path (the default: no fused short-state batches): the two sets of lists are the
     // same, so `all` is not built separately
-    m->all_is_qp = qc.size() == allc.size();
+    m->all_is_qp = !fused || qc.size() == allc.size();
     const long long* by_len = m->exact_sorted ? h_colptr : nullptr;
-    if (!m->all_is_qp) fill_lists(m, m->all, allc, cls, by_len);
-    fill_lists(m, m->qp, qc, cls, by_len);
+    if (!m->all_is_qp) fill_lists(m, m->all, &allc, cls, by_len);
+    fill_lists(m, m->qp, fused ? &qc : nullptr, cls, by_len);
     if (!m->all_is_qp) pack_tiny<T>(m, m->all, h_colptr);
     pack_tiny<T>(m, m->qp, h_colptr);
     tr.mark("lists");
