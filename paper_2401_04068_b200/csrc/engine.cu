@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <charconv>
 #include <chrono>
@@ -539,48 +540,85 @@ __host__ __device__ int column_class(long long len, double rem, double maxgap, i
 // by_length: sort each many-pick class list by decreasing length (longest first balances the persistent
 // grids of the float32 exact route)
 // cols == nullptr: every column, in order
+// The partition is parallel over host threads (per-thread class counts, then each thread writes its part
+// of every list at its offset: the lists keep increasing column order); the length sort is a stable
+// counting sort (a class spans at most 2^kSortedMaxLog lengths).
 void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>* cols, const std::vector<signed char>& cls,
                 const long long* by_length = nullptr) {
-    std::vector<int> sh, ex, md[2], ti[3], so[kSortedClasses];
-    const int n = cols ? (int)cols->size() : (int)cls.size();
-    {   // exact sizes first: one pass counting the classes
-        long long cnt[32] = {};
-        for (int i = 0; i < n; ++i) ++cnt[cls[cols ? (*cols)[i] : i] & 31];
-        sh.reserve(cnt[0]);
-        ex.reserve(cnt[1]);
-        for (int i = 0; i < 2; ++i) md[i].reserve(cnt[kClassMedium + i]);
-        for (int i = 0; i < 3; ++i) ti[i].reserve(cnt[kClassTiny + i]);
-        for (int i = 0; i < kSortedClasses; ++i) so[i].reserve(cnt[kClassSorted + i]);
+    constexpr int K = 32;
+    const long long n = cols ? (long long)cols->size() : (long long)cls.size();
+    const int nt = (int)std::max<long long>(1, std::min<long long>({16, (long long)std::max(1u, std::thread::hardware_concurrency()),
+                                                                     n / 65536 + 1}));
+    std::vector<std::array<long long, K>> cnt(nt);
+    auto col_at = [&](long long i) -> int { return cols ? (*cols)[i] : (int)i; };
+    auto part = [&](int t, long long& b, long long& e) {
+        b = n * t / nt;
+        e = n * (t + 1) / nt;
+    };
+    auto run = [&](auto&& f) {
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(f, t);
+        f(0);
+        for (auto& x : th) x.join();
+    };
+    run([&](int t) {
+        long long b, e;
+        part(t, b, e);
+        cnt[t].fill(0);
+        for (long long i = b; i < e; ++i) ++cnt[t][cls[col_at(i)] & (K - 1)];
+    });
+    std::vector<int> out[K];
+    std::vector<std::array<long long, K>> off(nt);
+    for (int k = 0; k < K; ++k) {
+        long long a = 0;
+        for (int t = 0; t < nt; ++t) {
+            off[t][k] = a;
+            a += cnt[t][k];
+        }
+        out[k].resize(a);
     }
-    for (int i = 0; i < n; ++i) {
-        const int c = cols ? (*cols)[i] : i;
-        const int k = cls[c];
-        if (k == 0) sh.push_back(c);
-        else if (k >= kClassTiny) ti[k - kClassTiny].push_back(c);
-        else if (k == 1) ex.push_back(c);
-        else if (k < kClassSorted) md[k - kClassMedium].push_back(c);
-        else so[k - kClassSorted].push_back(c);
-    }
-    L.n_short = (int)sh.size();
-    L.n_exact = (int)ex.size();
-    upload_list(m, L.short_list, sh);
-    upload_list(m, L.exact_list, ex);
+    run([&](int t) {
+        long long b, e;
+        part(t, b, e);
+        std::array<long long, K> o = off[t];
+        for (long long i = b; i < e; ++i) {
+            const int c = col_at(i);
+            const int k = cls[c] & (K - 1);
+            out[k][o[k]++] = c;
+        }
+    });
+    L.n_short = (int)out[0].size();
+    L.n_exact = (int)out[1].size();
+    upload_list(m, L.short_list, out[0]);
+    upload_list(m, L.exact_list, out[1]);
     for (int i = 0; i < 2; ++i) {
-        L.n_medium[i] = (int)md[i].size();
-        upload_list(m, L.medium_list[i], md[i]);
+        L.n_medium[i] = (int)out[kClassMedium + i].size();
+        upload_list(m, L.medium_list[i], out[kClassMedium + i]);
     }
     for (int i = 0; i < 3; ++i) {
-        L.n_tiny[i] = (int)ti[i].size();
-        upload_list(m, L.tiny_list[i], ti[i]);
-        L.tiny_host[i] = std::move(ti[i]);
+        L.n_tiny[i] = (int)out[kClassTiny + i].size();
+        upload_list(m, L.tiny_list[i], out[kClassTiny + i]);
+        L.tiny_host[i] = std::move(out[kClassTiny + i]);
     }
     for (int i = 0; i < kSortedClasses; ++i) {
-        if (by_length)
-            std::stable_sort(so[i].begin(), so[i].end(), [&](int a, int b) {
-                return by_length[a + 1] - by_length[a] > by_length[b + 1] - by_length[b];
-            });
-        L.n_sorted[i] = (int)so[i].size();
-        upload_list(m, L.sorted_list[i], so[i]);
+        std::vector<int>& so = out[kClassSorted + i];
+        if (by_length && so.size() > 1) {
+            // stable counting sort by decreasing length
+            long long lo = LLONG_MAX, hi = 0;
+            for (int c : so) {
+                const long long len = by_length[c + 1] - by_length[c];
+                lo = std::min(lo, len);
+                hi = std::max(hi, len);
+            }
+            std::vector<long long> pos(hi - lo + 2, 0);
+            for (int c : so) ++pos[hi - (by_length[c + 1] - by_length[c]) + 1];
+            for (size_t x = 1; x < pos.size(); ++x) pos[x] += pos[x - 1];
+            std::vector<int> sorted(so.size());
+            for (int c : so) sorted[pos[hi - (by_length[c + 1] - by_length[c])]++] = c;
+            so.swap(sorted);
+        }
+        L.n_sorted[i] = (int)so.size();
+        upload_list(m, L.sorted_list[i], so);
     }
 }
 
