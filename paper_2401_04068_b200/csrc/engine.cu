@@ -813,6 +813,7 @@ void build_schedule(rimdp_model* m, const long long* h_colptr) {
     const long long* by_len = m->exact_sorted ? h_colptr : nullptr;
     if (!m->all_is_qp) fill_lists(m, m->all, &allc, cls, by_len);
     fill_lists(m, m->qp, fused ? &qc : nullptr, cls, by_len);
+    tr.mark("fill");
     if (!m->all_is_qp) pack_tiny<T>(m, m->all, h_colptr);
     pack_tiny<T>(m, m->qp, h_colptr);
     tr.mark("lists");
