@@ -2323,7 +2323,8 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             if (lane == 31) wtot[wig] = em;
             __syncthreads(); // B2
             em -= fm;
-            for (int i = 0; i < wig; ++i) em += static_cast<unsigned>(wtot[i]);
+            // totals of the warps before this one: one load per lane and a warp reduction
+            em += __reduce_add_sync(kFull, lane < wig ? static_cast<unsigned>(wtot[lane]) : 0u);
             {
                 // truncation lost < 1 unit per entry, < L before any bucket
                 const double R = (double)r * sc, RL = R - (double)L;
@@ -2337,8 +2338,13 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
                         em += hist[bb];
                     }
                 }
-                if (blo >= 0) atomicMax(dw + 0, blo + 1);
-                if (bhi >= 0) atomicMax(dw + 1, bhi + 1);
+                // one shared atomic per warp (the whole block would otherwise hit the same two words)
+                const unsigned wlo = __reduce_max_sync(kFull, static_cast<unsigned>(blo + 1));
+                const unsigned whi = __reduce_max_sync(kFull, static_cast<unsigned>(bhi + 1));
+                if (lane == 0) {
+                    if (wlo > 0) atomicMax(dw + 0, static_cast<int>(wlo));
+                    if (whi > 0) atomicMax(dw + 1, static_cast<int>(whi));
+                }
             }
             __syncthreads(); // B3
             const int blo = dw[0] > 0 ? dw[0] - 1 : 0; // the first entry is always reached (rem > 0)
