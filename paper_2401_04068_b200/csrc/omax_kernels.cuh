@@ -2510,6 +2510,7 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
         const long long b = __ldg(colptr + c);
         const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
         const T r = __ldg(rem + c);
+        const T gm = __ldg(maxgap + c); // issued with the other metadata, not behind the column's loads
         const bool picks = r > T(0);
         int rw[E];
 #pragma unroll
@@ -2536,7 +2537,6 @@ omax_wbucket(int nlist, const int* __restrict__ list, const long long* __restric
 #pragma unroll
             for (int i = lane; i < B; i += 32) hist[i] = 0u;
             __syncwarp();
-            const T gm = __ldg(maxgap + c);
             const double sc = gm > T(0) ? 2147483648.0 / ((double)L * (double)gm) : 0.0;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
