@@ -215,6 +215,15 @@ struct rimdp_model {
     bool bucket = true;                       // columns > 256 entries: value buckets first (RIMDP_BUCKET=0: off)
     DevBuf fallback[kSortedClasses];          // per size class: [count A, count B, columns...] omax_bucket -> omax_select
     int fallback_parity[kSortedClasses] = {}; // which count the next omax_bucket launch of the class uses
+    // merged fallback list of one column pass (see begin_merged_fallback): [count A, count B, columns...]
+    DevBuf fb_all;
+    int fb_all_parity = 0;
+    bool fb_merge = false;                    // the class launchers append to fb_* and launch no fallback kernel
+    int* fbm_list = nullptr;
+    int* fbm_count = nullptr;
+    int* fbm_other = nullptr;
+    int fbm_cap = 0;                          // columns the merged list can hold (the pass's many-pick columns)
+    int fb_maxlg = 0;                         // largest size class that appended (0: no fallback kernel)
     int medium_blocks_per_sm = 3;             // omax_medium occupancy variant (RIMDP_MEDIUM_BLOCKS=4: <= 64 registers)
     int nstreams = 1;                         // column classes fanned out over this many streams (RIMDP_STREAMS)
     cudaStream_t side[kMaxSideStreams] = {};  // fork/join streams for concurrent column classes
@@ -1128,6 +1137,10 @@ struct FallbackSlots {
 };
 
 FallbackSlots fallback_slots(rimdp_model* m, int cls, int count) {
+    if (m->fb_merge) {
+        m->fb_maxlg = std::max(m->fb_maxlg, cls + kSortedMinLog);
+        return FallbackSlots{m->fbm_list, m->fbm_count, m->fbm_other};
+    }
     DevBuf& fbuf = m->fallback[cls];
     const size_t need = sizeof(int) * (size_t)(std::max(count, 1) + 2);
     if (fbuf.bytes < need) {
@@ -1156,6 +1169,23 @@ ExactDotKernel exact_dot_kernel() {
     return g == 1 ? exact_dot : exact_dotg<2>;
 }
 
+// The float32 exact route's fallback: the bitonic exact kernel over the listed columns (<= 2^LG entries)
+template <bool P, int LG>
+void launch_exact_fallback(rimdp_model* m, int count, const int* list, const int* count_dev, const float* V,
+                           float* q, Ctl* ctl) {
+    using SS = SortedShape<LG>;
+    auto kf = omax_sorted<float, P, LG, true>;
+    static bool fconf[64] = {};
+    const int dev = m->device & 63;
+    if (!fconf[dev]) {
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::template smem<float>()));
+        fconf[dev] = true;
+    }
+    launch_pdl(m->pdl_wait_ok(), kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
+               list, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(), m->gap.as<float>(),
+               m->rem.as<float>(), V, q, (const Ctl*)ctl, count_dev);
+}
+
 template <class T, bool P, int LG>
 void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* V, T* q, Ctl* ctl) {
     if constexpr (std::is_same<T, float>::value && LG <= 8) {
@@ -1176,16 +1206,7 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
         launch_pdl(m->pdl_now, k, grid_for(count, Sh::W, m->sm_count, per_sm[dev]), Sh::W * 32, Sh::smem(), m->ls,
                    count, list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(),
                    m->gap.as<float>(), m->rem.as<float>(), V, q, f.list, f.count, f.other, (const Ctl*)ctl);
-        using SS = SortedShape<LG>;
-        auto kf = omax_sorted<float, P, LG, true>;
-        static bool fconf[64] = {};
-        if (!fconf[dev]) {
-            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::template smem<float>()));
-            fconf[dev] = true;
-        }
-        launch_pdl(m->pdl_wait_ok(), kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
-                   (const int*)f.list, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(),
-                   m->gap.as<float>(), m->rem.as<float>(), V, q, (const Ctl*)ctl, (const int*)f.count);
+        if (!m->fb_merge) launch_exact_fallback<P, LG>(m, count, f.list, f.count, V, q, ctl);
     } else if constexpr (std::is_same<T, float>::value) {
         using Sh = ExactShape<LG>;
         auto ks = exact_sort<P, LG>;
@@ -1218,16 +1239,7 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
                    (const unsigned short*)m->xs_pos.as<unsigned short>(), (const float*)m->xs_val.as<float>(), q,
                    (const Ctl*)ctl);
         // overflowed columns: the bitonic exact kernel (after exact_dot, which wrote placeholders for them)
-        using SS = SortedShape<LG>;
-        auto kf = omax_sorted<float, P, LG, true>;
-        static bool fconf[64] = {};
-        if (!fconf[dev]) {
-            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::template smem<float>()));
-            fconf[dev] = true;
-        }
-        launch_pdl(m->pdl_wait_ok(), kf, std::min(count, m->sm_count), SS::threads, SS::template smem<float>(), m->ls, count,
-                   (const int*)f.list, m->colptr.as<long long>(), m->rows.as<int>(), m->lower.as<float>(),
-                   m->gap.as<float>(), m->rem.as<float>(), V, q, (const Ctl*)ctl, (const int*)f.count);
+        if (!m->fb_merge) launch_exact_fallback<P, LG>(m, count, f.list, f.count, V, q, ctl);
     } else {
         launch_sorted_class<T, P, LG, true>(m, count, list, V, q, ctl);
     }
@@ -1254,7 +1266,7 @@ void launch_bucket_class(rimdp_model* m, int count, const DevBuf& list, const T*
     launch_pdl(m->pdl_now, k, blocks, Sh::NT, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
                m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V, q, ctl,
                f.list, f.count, f.other, m->vrange_cur);
-    launch_select_class<T, P, LG>(m, count, f.list, V, q, ctl, f.count);
+    if (!m->fb_merge) launch_select_class<T, P, LG>(m, count, f.list, V, q, ctl, f.count);
 }
 
 // Many-pick columns of 33 .. 256 entries: warp-per-column value buckets,
@@ -1274,7 +1286,7 @@ void launch_wbucket_class(rimdp_model* m, int count, const DevBuf& list, const T
     launch_pdl(m->pdl_now, k, blocks, Sh::W * 32, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
                m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V, q, ctl,
                f.list, f.count, f.other, m->vrange_cur);
-    launch_select_class<T, P, LG>(m, count, f.list, V, q, ctl, f.count);
+    if (!m->fb_merge) launch_select_class<T, P, LG>(m, count, f.list, V, q, ctl, f.count);
 }
 
 // Many-pick long columns by size class: weighted quickselect (omax_select,
@@ -1501,6 +1513,58 @@ void launch_value_range(rimdp_model* m, const ColumnLists& L, const T* V) {
     m->vrange_cur = slot;
 }
 
+// Merged fallback of one column pass.  Every many-pick class kernel (bucket, wbucket, exact) appends the
+// columns it could not finish to one list, and a single fallback kernel sized for the largest class that
+// ran (omax_select, or the bitonic exact kernel on the float32 route) processes them after all classes:
+// one launch instead of one per class (C5: 7, each a full wait on its predecessor; they find the list
+// empty almost always).  The counters alternate between passes like the per-class ones.
+void begin_merged_fallback(rimdp_model* m, const ColumnLists& L) {
+    long long total = 0;
+    for (int i = 0; i < kSortedClasses; ++i) total += L.n_sorted[i];
+    m->fb_maxlg = 0;
+    m->fb_merge = total > 0 && !m->bitonic && (m->bucket || m->exact_sorted);
+    if (!m->fb_merge) return;
+    const size_t need = sizeof(int) * (size_t)(total + 2);
+    if (m->fb_all.bytes < need) {
+        m->fb_all.ensure(need);
+        CK(cudaMemsetAsync(m->fb_all.p, 0, 2 * sizeof(int), m->ls));
+    }
+    int* base = m->fb_all.as<int>();
+    m->fbm_list = base + 2;
+    m->fbm_count = base + m->fb_all_parity;
+    m->fbm_other = base + (m->fb_all_parity ^ 1);
+    m->fbm_cap = (int)total;
+    m->fb_all_parity ^= 1;
+}
+
+template <class T, bool P, int LG = kSortedMinLog>
+void launch_merged_fallback_lg(rimdp_model* m, const T* V, T* q, Ctl* ctl) {
+    if constexpr (LG <= kSortedMaxLog) {
+        if (m->fb_maxlg == LG) {
+            if constexpr (std::is_same<T, float>::value) {
+                if (m->exact_sorted) {
+                    launch_exact_fallback<P, LG>(m, m->fbm_cap, m->fbm_list, m->fbm_count, V, q, ctl);
+                    return;
+                }
+            }
+            launch_select_class<T, P, LG>(m, m->fbm_cap, m->fbm_list, V, q, ctl, m->fbm_count);
+            return;
+        }
+        launch_merged_fallback_lg<T, P, LG + 1>(m, V, q, ctl);
+    }
+}
+
+template <class T>
+void end_merged_fallback(rimdp_model* m, bool pess, const T* V, T* q, Ctl* ctl) {
+    if (m->fb_merge && m->fb_maxlg > 0) {
+        if (pess)
+            launch_merged_fallback_lg<T, true>(m, V, q, ctl);
+        else
+            launch_merged_fallback_lg<T, false>(m, V, q, ctl);
+    }
+    m->fb_merge = false;
+}
+
 template <class T>
 void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
     launch_value_range<T>(m, L, V);
@@ -1533,10 +1597,12 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
     if (L.n_tiny[1] > 0) { f.pick(); launch_tiny<T, 8>(m, L, 1, V, q, ctl, pess); }
     if (L.n_tiny[0] > 0) { f.pick(); launch_tiny<T, 4>(m, L, 0, V, q, ctl, pess); }
     if (!f.on) {
+        begin_merged_fallback(m, L);
         if (pess)
             launch_sorted<T, true>(m, L, V, q, ctl);
         else
             launch_sorted<T, false>(m, L, V, q, ctl);
+        end_merged_fallback<T>(m, pess, V, q, ctl);
     }
 }
 
