@@ -133,16 +133,19 @@ struct DevBuf {
 // <= 64 / <= 128 entries) or the exact warp kernel (omax_long, any length);
 // the rest -> one CTA per column, sorted (omax_sorted), by power-of-two size
 // class 2^6 .. 2^13.
+// tiny classes: <= 4, <= 8, <= 16 entries (4 / 8 / 16 lanes per column), and single entries (1 lane)
+constexpr int kTinyClasses = 4;
 constexpr int kSortedMinLog = 6, kSortedMaxLog = 13, kSortedClasses = kSortedMaxLog - kSortedMinLog + 1;
 constexpr double kExactPickBudget = 4.0;
 
 struct ColumnLists {
-    DevBuf short_list, exact_list, medium_list[2], tiny_list[3], sorted_list[kSortedClasses];
-    int n_short = 0, n_exact = 0, n_medium[2] = {}, n_tiny[3] = {}, n_sorted[kSortedClasses] = {};
+    DevBuf short_list, exact_list, medium_list[2], tiny_list[kTinyClasses], sorted_list[kSortedClasses];
+    int n_short = 0, n_exact = 0, n_medium[2] = {}, n_tiny[kTinyClasses] = {}, n_sorted[kSortedClasses] = {};
     // tiny classes packed in list order (pack_columns): begins [n + 1], rem [n], rows / lower / gap
-    DevBuf tiny_beg[3], tiny_rem[3], tiny_rows[3], tiny_lower[3], tiny_gap[3];
-    bool tiny_packed[3] = {};
-    std::vector<int> tiny_host[3]; // the lists on the host, until packed
+    DevBuf tiny_beg[kTinyClasses], tiny_rem[kTinyClasses], tiny_rows[kTinyClasses], tiny_lower[kTinyClasses],
+        tiny_gap[kTinyClasses];
+    bool tiny_packed[kTinyClasses] = {};
+    std::vector<int> tiny_host[kTinyClasses]; // the lists on the host, until packed
     int total_sorted() const {
         int t = 0;
         for (int i = 0; i < kSortedClasses; ++i) t += n_sorted[i];
@@ -520,9 +523,10 @@ int long_mode() {
 // Class of one column given its length, remainder and largest gap.
 //   0: short   1: exact long   2: medium (E = 2)   3: medium (E = 4)
 //   4 + i: sorted, size class 2^(kSortedMinLog + i)
-//   kClassTiny + i: <= 4 << i entries (i = 0, 1, 2), several columns per warp
+//   kClassTiny + i: <= 4 << i entries (i = 0, 1, 2), several columns per warp; kClassTiny + 3: one entry
 constexpr int kClassMedium = 2, kClassSorted = 4, kClassTiny = 16;
 __host__ __device__ int column_class(long long len, double rem, double maxgap, int mode) {
+    if (len == 1) return kClassTiny + 3; // one lane per column (32 per warp step)
     if (len <= 4) return kClassTiny;
     if (len <= 8) return kClassTiny + 1;
     if (len <= 16) return kClassTiny + 2;
@@ -604,7 +608,7 @@ void fill_lists(rimdp_model* m, ColumnLists& L, const std::vector<int>* cols, co
         L.n_medium[i] = (int)out[kClassMedium + i].size();
         upload_list(m, L.medium_list[i], out[kClassMedium + i]);
     }
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < kTinyClasses; ++i) {
         L.n_tiny[i] = (int)out[kClassTiny + i].size();
         upload_list(m, L.tiny_list[i], out[kClassTiny + i]);
         L.tiny_host[i] = std::move(out[kClassTiny + i]);
@@ -651,7 +655,7 @@ bool tiny_pack_enabled() {
 
 template <class T>
 void pack_tiny(rimdp_model* m, ColumnLists& L, const long long* h_colptr) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < kTinyClasses; ++i) {
         std::vector<int>& lst = L.tiny_host[i];
         L.tiny_packed[i] = false;
         if (lst.empty() || !tiny_pack_enabled()) {
@@ -1462,7 +1466,7 @@ struct ClassFanout {
 
 int column_classes(const ColumnLists& L) {
     int k = (L.n_short > 0) + (L.n_exact > 0) + (L.n_medium[0] > 0) + (L.n_medium[1] > 0);
-    for (int i = 0; i < 3; ++i) k += L.n_tiny[i] > 0;
+    for (int i = 0; i < kTinyClasses; ++i) k += L.n_tiny[i] > 0;
     for (int i = 0; i < kSortedClasses; ++i) k += L.n_sorted[i] > 0;
     return k;
 }
@@ -1596,6 +1600,7 @@ void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl*
     if (L.n_tiny[2] > 0) { f.pick(); launch_tiny<T, 16>(m, L, 2, V, q, ctl, pess); }
     if (L.n_tiny[1] > 0) { f.pick(); launch_tiny<T, 8>(m, L, 1, V, q, ctl, pess); }
     if (L.n_tiny[0] > 0) { f.pick(); launch_tiny<T, 4>(m, L, 0, V, q, ctl, pess); }
+    if (L.n_tiny[3] > 0) { f.pick(); launch_tiny<T, 1>(m, L, 3, V, q, ctl, pess); }
     if (!f.on) {
         begin_merged_fallback(m, L);
         if (pess)
@@ -1694,8 +1699,8 @@ void launch_iteration(rimdp_model* m, long long k, int* chosen, int chosen_td) {
 
 int kernels_per_iteration(const rimdp_model* m) {
     int k = (m->nbatch > 0) + (m->qp.n_short > 0) + (m->qp.n_exact > 0) + (m->nlong_states > 0) +
-            (m->qp.n_medium[0] > 0) + (m->qp.n_medium[1] > 0) + (m->qp.n_tiny[0] > 0) + (m->qp.n_tiny[1] > 0) +
-            (m->qp.n_tiny[2] > 0);
+            (m->qp.n_medium[0] > 0) + (m->qp.n_medium[1] > 0);
+    for (int i = 0; i < kTinyClasses; ++i) k += m->qp.n_tiny[i] > 0;
     for (int i = 0; i < kSortedClasses; ++i) k += m->qp.n_sorted[i] > 0;
     return k + (m->x.connected ? 1 : 0);
 }
@@ -2085,7 +2090,7 @@ int rimdp_model_info_get(rimdp_model* m, rimdp_model_info* o) {
     o->num_infeasible_columns = (int)m->infeasible_cols.size();
     o->device_bytes = m->device_bytes;
     const ColumnLists& all = m->all_lists();
-    o->short_columns = all.n_short + all.n_tiny[0] + all.n_tiny[1] + all.n_tiny[2];
+    o->short_columns = all.n_short + all.n_tiny[0] + all.n_tiny[1] + all.n_tiny[2] + all.n_tiny[3];
     o->mid_columns = all.n_exact + all.n_medium[0] + all.n_medium[1];
     o->long_columns = all.total_sorted();
     return RIMDP_OK;
