@@ -222,6 +222,7 @@ struct rimdp_model {
     DevBuf fb_all;
     int fb_all_parity = 0;
     bool fb_merge = false;                    // the class launchers append to fb_* and launch no fallback kernel
+    unsigned* work_cur = nullptr;             // the column pass's work counters (launch_columns)
     int* fbm_list = nullptr;
     int* fbm_count = nullptr;
     int* fbm_other = nullptr;
@@ -1269,7 +1270,8 @@ void launch_bucket_class(rimdp_model* m, int count, const DevBuf& list, const T*
     const int blocks = grid_for(count, 1, m->sm_count, per_sm[dev]);
     launch_pdl(m->pdl_now, k, blocks, Sh::NT, smem, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
                m->rows.as<int>(), m->lower.as<T>(), m->gap.as<T>(), m->rem.as<T>(), m->maxgap.as<T>(), V, q, ctl,
-               f.list, f.count, f.other, m->vrange_cur);
+               f.list, f.count, f.other, m->vrange_cur,
+               m->work_cur ? m->work_cur + kWorkSorted + (LG - kSortedMinLog) : nullptr);
     if (!m->fb_merge) launch_select_class<T, P, LG>(m, count, f.list, V, q, ctl, f.count);
 }
 
@@ -1571,6 +1573,7 @@ void end_merged_fallback(rimdp_model* m, bool pess, const T* V, T* q, Ctl* ctl) 
 
 template <class T>
 void launch_columns(rimdp_model* m, const ColumnLists& L, const T* V, T* q, Ctl* ctl, bool pess, unsigned* work) {
+    m->work_cur = work;
     launch_value_range<T>(m, L, V);
     if (m->gate_needed && !m->vrange_cur) { // value_range (plain launch) is the gate when it runs
         pdl_gate<<<1, 32, 0, m->stream>>>();

@@ -2211,7 +2211,8 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             const int* __restrict__ rows, const T* __restrict__ lower, const T* __restrict__ gap,
             const T* __restrict__ rem, const T* __restrict__ maxgap, const T* __restrict__ V, T* __restrict__ q,
             const Ctl* __restrict__ ctl, int* __restrict__ fallback, int* __restrict__ nfallback,
-            int* __restrict__ other_nfallback, const unsigned long long* __restrict__ vrange) {
+            int* __restrict__ other_nfallback, const unsigned long long* __restrict__ vrange,
+            unsigned* __restrict__ work) {
     using N = Num<T>;
     using Bits = typename N::Bits;
     using Sh = BucketShape<LG, T>;
@@ -2250,8 +2251,13 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
     if (t < 8) dwb[t] = 0;
     __syncthreads();
     unsigned par = 0;
+    // columns are taken dynamically (work counter; the first one per CTA is blockIdx.x): thread 0 claims
+    // the CTA's next column while this one loads, every thread reads it behind B1 (alternating slots)
+    __shared__ int next_slot[2];
+    int next_item = nlist;
 
-    for (int item = blockIdx.x; item < nlist; item += gridDim.x) {
+    for (int item = blockIdx.x; item < nlist; item = next_item) {
+        if (t == 0) next_slot[par] = work ? static_cast<int>(gridDim.x + atomicAdd(work, 1u)) : item + static_cast<int>(gridDim.x);
         const int c = __ldg(list + item);
         const long long b = __ldg(colptr + c);
         const int L = static_cast<int>(__ldg(colptr + c + 1) - b);
@@ -2298,6 +2304,7 @@ omax_bucket(int nlist, const int* __restrict__ list, const long long* __restrict
             }
         }
         __syncthreads(); // B1: histogram complete
+        next_item = next_slot[par];
         {   // the next column's buffers: their last readers (the previous column) are past B1
             unsigned* oh = hbuf + (par ^ 1u) * B;
             for (int i = t; i < B; i += NT) oh[i] = 0u;
@@ -2678,7 +2685,8 @@ struct ActionArgs {
     const PeerTable* peers;        // sharded solve with peer exchange, else null
 };
 
-constexpr int kWorkKinds = 4;      // 0: omax_short (q path), 1: bellman_short, 2/3: omax_medium E = 2/4
+constexpr int kWorkSorted = 4;     // work counters of the many-pick size classes 2^6 .. 2^13 (omax_bucket)
+constexpr int kWorkKinds = 12;     // 0: omax_short (q path), 1: bellman_short, 2/3: omax_medium E = 2/4, 4..11: classes
 
 __device__ __forceinline__ const int* forced_row(const ActionArgs& a) {
     return a.forced ? a.forced + (a.forced_td ? (a.horizon - a.k) * (long long)a.n : 0) : nullptr;
