@@ -1168,7 +1168,7 @@ int exact_dot_group() {
     return g;
 }
 using ExactDotKernel = void (*)(int, const int*, const long long*, const float*, const float*, float*,
-                                const unsigned short*, const float*, float*, const Ctl*);
+                                const unsigned short*, const float*, float*, const Ctl*, unsigned*);
 ExactDotKernel exact_dot_kernel() {
     const int g = exact_dot_group();
     return g == 1 ? exact_dot : exact_dotg<2>;
@@ -1236,13 +1236,14 @@ void launch_exact_class(rimdp_model* m, int count, const DevBuf& list, const T* 
         launch_pdl(m->pdl_now, ks, grid_for(count, 1, m->sm_count, per_sm[dev]), Sh::NT, Sh::smem(), m->ls, count,
                    list.as<int>(), m->colptr.as<long long>(), m->rows.as<int>(), m->gap.as<float>(), V,
                    m->xs_gap.as<float>(), m->xs_pos.as<unsigned short>(), m->xs_val.as<float>(), f.list, f.count,
-                   f.other, (const Ctl*)ctl, m->vrange_cur);
+                   f.other, (const Ctl*)ctl, m->vrange_cur,
+                   m->work_cur ? m->work_cur + kWorkSorted + (LG - kSortedMinLog) : nullptr);
         const int G = exact_dot_group();
         launch_pdl(m->pdl_wait_ok(), exact_dot_kernel(), grid_for((count + G - 1) / G, kExactDotWarps, m->sm_count, dot_per_sm[dev]),
                    kExactDotWarps * 32, 0, m->ls, count, list.as<int>(), m->colptr.as<long long>(),
                    m->lower.as<float>(), m->rem.as<float>(), m->xs_gap.as<float>(),
                    (const unsigned short*)m->xs_pos.as<unsigned short>(), (const float*)m->xs_val.as<float>(), q,
-                   (const Ctl*)ctl);
+                   (const Ctl*)ctl, m->work_cur ? m->work_cur + kWorkDot + (LG - kSortedMinLog) : nullptr);
         // overflowed columns: the bitonic exact kernel (after exact_dot, which wrote placeholders for them)
         if (!m->fb_merge) launch_exact_fallback<P, LG>(m, count, f.list, f.count, V, q, ctl);
     } else {

@@ -88,7 +88,7 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
            const int* __restrict__ rows, const float* __restrict__ gap, const float* __restrict__ V,
            float* __restrict__ S, unsigned short* __restrict__ POS, float* __restrict__ VS,
            int* __restrict__ fb_list, int* __restrict__ fb_count, int* __restrict__ fb_other,
-           const Ctl* __restrict__ ctl, const unsigned long long* __restrict__ vrange) {
+           const Ctl* __restrict__ ctl, const unsigned long long* __restrict__ vrange, unsigned* __restrict__ work) {
     using Sh = ExactShape<LG>;
     constexpr int N = Sh::N, NT = Sh::NT, E = Sh::E;
     pdl_enter_class(ctl);
@@ -113,7 +113,12 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
     const float wmin = kPess ? vlo : -vhi, wmax = kPess ? vhi : -vlo;
     const float width = __fsub_rn(wmax, wmin);
     const float scale = width > 0.f && width < 3.0e38f ? __fdiv_rn(static_cast<float>(N), width) : 0.f;
-    for (int item = blockIdx.x; item < nlist; item += gridDim.x) {
+    // columns are taken dynamically (work counter; the first one per CTA is blockIdx.x): thread 0 claims
+    // the CTA's next column at the start of this one, every thread reads it behind the histogram barrier
+    __shared__ int next_slot[2];
+    int next_item = nlist, par = 0;
+    for (int item = blockIdx.x; item < nlist; item = next_item, par ^= 1) {
+        if (tid == 0) next_slot[par] = work ? static_cast<int>(gridDim.x + atomicAdd(work, 1u)) : item + static_cast<int>(gridDim.x);
         const int c = list[item];
         const long long b0 = colptr[c];
         const int L = static_cast<int>(colptr[c + 1] - b0);
@@ -150,6 +155,7 @@ exact_sort(int nlist, const int* __restrict__ list, const long long* __restrict_
             }
         }
         __syncthreads();
+        next_item = next_slot[par];
         block_exclusive_scan<NT, E>(cnt, wsum);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(kExactDotWarps * 32)
 exact_dot(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
           const float* __restrict__ lower, const float* __restrict__ rem, float* __restrict__ S,
           const unsigned short* __restrict__ POS, const float* __restrict__ VS, float* __restrict__ q,
-          const Ctl* __restrict__ ctl) {
+          const Ctl* __restrict__ ctl, unsigned* __restrict__ /*work: static assignment*/) {
     using N_ = Num<float>;
     pdl_enter();
     if (ctl && *reinterpret_cast<const volatile int*>(&ctl->done)) return;
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(kExactDotWarps * 32)
 exact_dotg(int nlist, const int* __restrict__ list, const long long* __restrict__ colptr,
            const float* __restrict__ lower, const float* __restrict__ rem, float* __restrict__ S,
            const unsigned short* __restrict__ POS, const float* __restrict__ VS, float* __restrict__ q,
-           const Ctl* __restrict__ ctl) {
+           const Ctl* __restrict__ ctl, unsigned* __restrict__ work) {
     using N_ = Num<float>;
     constexpr int U = 8;       // entries per lane per chunk
     constexpr int LPC = 32 / G; // lanes per column
@@ -389,7 +395,13 @@ exact_dotg(int nlist, const int* __restrict__ list, const long long* __restrict_
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, h = lane / LPC, hl = lane % LPC;
     float* sb = buf[w][h];
     const int ngroups = (nlist + G - 1) / G;
-    for (int pr = blockIdx.x * kExactDotWarps + w; pr < ngroups; pr += gridDim.x * kExactDotWarps) {
+    // column groups are taken dynamically (work counter; the first one per warp is its index): lane 0
+    // claims the warp's next group at the start of this one, the warp reads it after the walk
+    const int nwarps = gridDim.x * kExactDotWarps;
+    int next_pr = ngroups;
+    for (int pr = blockIdx.x * kExactDotWarps + w; pr < ngroups; pr = next_pr) {
+        unsigned claim = 0;
+        if (lane == 0) claim = work ? static_cast<unsigned>(nwarps) + atomicAdd(work, 1u) : static_cast<unsigned>(pr + nwarps);
         const int item = G * pr + h;
         const bool valid = item < nlist;
         const int c = valid ? list[item] : 0;
@@ -462,6 +474,7 @@ exact_dotg(int nlist, const int* __restrict__ list, const long long* __restrict_
                 walking = false;
             }
         }
+        next_pr = static_cast<int>(__shfl_sync(kFull, claim, 0));
         // ---- row-order expectation (omax.hpp:169-173), CH products at a time per group ----
         int Lmax = L;
 #pragma unroll
@@ -556,6 +569,7 @@ exact_warp(int nlist, const int* __restrict__ list, const long long* __restrict_
     float* xb = reinterpret_cast<float*>(base);                       // dot staging, after the sort
     unsigned* cnt = reinterpret_cast<unsigned*>(base + (size_t)N * 8);
     float* S = reinterpret_cast<float*>(base + (size_t)N * 8 + (size_t)(N + 4) * 4);
+    // static assignment (a dynamic claim per column, as exact_sort, measured no better for warp kernels)
     for (int item = blockIdx.x * W + w; item < nlist; item += gridDim.x * W) {
         const int c = list[item];
         const long long b0 = colptr[c];
