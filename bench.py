@@ -119,6 +119,11 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a few hundred ms to start: wait for its first sample (at most 3 s), so that a
+            # short timed region (C2: ~20 ms) is covered by the 20 ms sampling
+            t_end = time.perf_counter() + 3.0
+            while not self.lines and time.perf_counter() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
